@@ -1,0 +1,128 @@
+/* eritile_gpu.h — C ABI of the B200 Fock-build engine (drop-in boundary).
+ *
+ * The reference (arxiv 2412.13203, proj/include/eritile/) is a header-only
+ * C++20 library with no executor; the executor contract it specifies is
+ *   eval_block(QuadBlock, ExecutionPlan, D, Accumulator&)
+ *   build_g(blocks, plans, D, mode) -> G
+ * called once per SCF iteration by scf_iterate. This ABI
+ * replaces that contract with plain pointers and sizes; every entry point
+ * cites the reference interface it stands in for. The C++ wrapper with the
+ * reference's names and exception behaviour is include/eritile/executor.hpp.
+ *
+ * Conventions: matrices are N x N row-major FP64, caller-owned, N =
+ * basis_dimension (molecule.hpp:193-197) in expand_functions order
+ * (molecule.hpp:185-191; components x-major, molecule.hpp:176-183). Inputs
+ * are copied at call time. Every function returns 0 on success and a
+ * negative code on failure; eritile_gpu_last_error() describes it. There is
+ * no CPU fallback: without a CUDA device eritile_gpu_create fails.
+ */
+#ifndef ERITILE_GPU_H
+#define ERITILE_GPU_H
+#include <stddef.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct eritile_gpu eritile_gpu;
+
+enum {
+  ERITILE_OK = 0,
+  ERITILE_ERR_ARG = -1,     /* std::invalid_argument in the reference */
+  ERITILE_ERR_PARSE = -2,   /* eritile::ParseError (molecule.hpp:72-74) */
+  ERITILE_ERR_CUDA = -3,    /* device failure / no device */
+  ERITILE_ERR_STATE = -4,   /* call order (e.g. build_jk before set_screening) */
+  ERITILE_ERR_DOMAIN = -5   /* std::domain_error (boys.hpp:48-50) */
+};
+
+typedef struct eritile_gpu_stats {
+  int nbf, nshells, npairs, nclasses;
+  long long quartets;        /* surviving canonical quartets on this rank */
+  long long prim_quartets;   /* surviving primitive quartets on this rank */
+  long long work_items;      /* warp tasks on this rank */
+  double model_flops;        /* SURVEY.md §8d F_c summed over classes (this rank) */
+  double last_build_ms;      /* device time of the last build_jk (CUDA events) */
+  double last_schwarz_ms;
+  int gpu_launches_last_build; /* kernels launched by the last build */
+} eritile_gpu_stats;
+
+/* Create a context on CUDA device `device`. Fails if no device. */
+int eritile_gpu_create(int device, eritile_gpu** out);
+void eritile_gpu_destroy(eritile_gpu* ctx);
+const char* eritile_gpu_last_error(const eritile_gpu* ctx);
+
+/* parse_xyz (molecule.hpp:105-158) + BasisSetTable::parse (basis_set.hpp:
+ * 33-84) + attach_basis (basis_set.hpp:127-155). */
+int eritile_gpu_load_molecule(eritile_gpu* ctx, const char* xyz_text, const char* basis_text);
+/* Alternative: already-normalised shells (Shell, molecule.hpp:39-50):
+ * L[s], K[s], center[3s..], atom[s]; exponents/coefficients concatenated. */
+int eritile_gpu_load_shells(eritile_gpu* ctx, int nshell, const int* L, const int* K,
+                            const double* center, const int* atom, const double* exps,
+                            const double* coefs, int natoms, const int* Z, const double* pos);
+int eritile_gpu_nbf(const eritile_gpu* ctx);
+/* Shell table after attach_basis: L, contraction degree, first basis
+ * function (expand_functions order, molecule.hpp:185-191). */
+int eritile_gpu_shell_info(const eritile_gpu* ctx, int* L, int* K, int* bf_off);
+int eritile_gpu_nshells(const eritile_gpu* ctx);
+int eritile_gpu_nelectrons(const eritile_gpu* ctx);
+double eritile_gpu_nuclear_repulsion(const eritile_gpu* ctx);
+
+/* build_pairs (block.hpp:52-103): all S(S+1)/2 pairs, kappa screen
+ * |coef|*kappa < kappa_screen drops primitive pairs (0 = off), upload. */
+int eritile_gpu_build_pairs(eritile_gpu* ctx, double kappa_screen);
+int eritile_gpu_npairs(const eritile_gpu* ctx);
+/* Reference pair-store order: shells (i<=j) of pair x, x < npairs. */
+int eritile_gpu_pair_shells(const eritile_gpu* ctx, int* i, int* j);
+
+/* Schwarz diagonal on the GPU; Q per pair in reference pair-store order
+ * (Q may be NULL). Not in the reference. */
+int eritile_gpu_schwarz(eritile_gpu* ctx, double* Q);
+/* Override Q (reference order) — used to share one Q with a checker. */
+int eritile_gpu_set_schwarz(eritile_gpu* ctx, const double* Q);
+
+/* Multi-GPU sharding: this context evaluates the work items of shard
+ * `rank` of `nranks` (deterministic; set before set_screening). */
+int eritile_gpu_set_shard(eritile_gpu* ctx, int rank, int nranks);
+/* Build the screened quartet work lists: keep (x,y) iff Q_x*Q_y >= tau
+ * (tau <= 0: no screening). Blocks are class- and contraction-sorted
+ * (Permutation, block.hpp:115-150 / PAPER.md:223-250). */
+int eritile_gpu_set_screening(eritile_gpu* ctx, double tau);
+long long eritile_gpu_num_quartets(const eritile_gpu* ctx);
+/* Export this rank's canonical quartet list as reference pair-store index
+ * pairs (x <= y), sorted ascending by (x, y). Returns the count. */
+long long eritile_gpu_quartets(const eritile_gpu* ctx, int* xs, int* ys, long long cap);
+
+/* build_g's J/K half: true Coulomb J and exchange K for a
+ * symmetric density D (G = 2J - K for RHF). Host buffers; includes H2D of D
+ * and D2H of J, K. Single rank: complete result. */
+int eritile_gpu_build_jk(eritile_gpu* ctx, const double* D, double* J, double* K);
+/* Device-resident variant for multi-GPU: D, accumulators are device pointers
+ * on this context's device; JKacc is 2*N*N doubles (Jacc ‖ Kacc, zeroed by
+ * the call) holding this rank's unsymmetrised partial sums, to be summed
+ * across ranks (one allreduce) and then passed to eritile_gpu_finalize.
+ * stream = cudaStream_t (NULL = context stream). */
+int eritile_gpu_build_jk_partial_device(eritile_gpu* ctx, const double* dD, double* dJKacc,
+                                        void* stream);
+int eritile_gpu_finalize_device(eritile_gpu* ctx, const double* dJKacc, double* dJ, double* dK,
+                                void* stream);
+int eritile_gpu_build_jk_device(eritile_gpu* ctx, const double* dD, double* dJ, double* dK,
+                                void* stream);
+
+/* One-electron S, T, V on the host; N x N. */
+int eritile_gpu_one_electron(eritile_gpu* ctx, double* S, double* T, double* V);
+
+/* boys (boys.hpp:46-54) evaluated by the device routine for n arguments. */
+int eritile_gpu_boys(eritile_gpu* ctx, int m_max, const double* T, int n, double* F);
+/* Scaled integrals of one quartet of reference pairs (x, y) in the reference
+ * component order a-major over (i,j,k,l) of pair x=(i,j), y=(k,l). */
+int eritile_gpu_eri_quartet(eritile_gpu* ctx, int x, int y, double* out);
+
+int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out);
+/* Plan statistics of the generated class kernels, i < num_classes:
+ * la lb lc ld max_m ops prim_terms base contract hrr_terms. */
+int eritile_gpu_num_classes(void);
+int eritile_gpu_class_info(int i, int* out10);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

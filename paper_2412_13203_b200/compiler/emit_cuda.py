@@ -1,0 +1,236 @@
+"""Emit per-class FP64 sm_100a device code from the Alg. 1 plans.
+
+For every canonical ERI class (La>=Lb, Lc>=Ld, bra pair class >= ket pair
+class in the key (L1+L2, L1, L2)) this writes ``csrc/generated/cls_<id>.cu``
+holding
+
+* ``struct Cls<id>``: compile-time sizes plus ``eri()``, the straight-line
+  evaluation of one contracted quartet: per primitive quartet the binding
+  (SPEC.md:290,316), the Boys values, the primitive (vertical) segment of the
+  plan and the fold into contracted accumulators; then the contracted
+  (horizontal) segment and the a-major target order (compiler.hpp:131-147,
+  dag.hpp:221-229). Registers are SSA values; nvcc allocates them.
+* explicit instantiations of the JK and Schwarz kernels of csrc/jk_kernels.cuh
+  and C launchers registered in ``csrc/generated/registry.cpp``.
+
+The plan is compiled in whichever orientation (bra|ket) or (ket|bra) has
+fewer operations; targets are remapped at emission time so the device
+function always returns values in the kernel's (bra|ket) a-major order.
+The contraction weight and the 2 pi^(5/2)/(pq sqrt(p+q)) kappa_ab kappa_cd
+prefactor are folded into one per-primitive-pair scalar U (csrc/host), so
+the boundary fold is ``t += r``.
+"""
+from __future__ import annotations
+
+import os
+from pathlib import Path
+from typing import Dict, List, Tuple
+
+from .dag import (AB, CD, I2P, I2PQ, I2Q, ITP_RP, ITQ_RQ, PA, PB, QC, QD, UNIT, WP, WQ,
+                  compile_class, components, is_base)
+
+PAIR_CLASSES_L2 = [(0, 0), (1, 0), (1, 1), (2, 0), (2, 1), (2, 2)]
+
+
+def pair_classes(lmax: int) -> List[Tuple[int, int]]:
+    out = [(a, b) for a in range(lmax + 1) for b in range(a + 1)]
+    return sorted(out, key=lambda t: (t[0] + t[1], t[0], t[1]))
+
+
+def canonical_classes(lmax: int) -> List[Tuple[int, int, int, int]]:
+    pcs = pair_classes(lmax)
+    out = []
+    for i, a in enumerate(pcs):
+        for b in pcs[: i + 1]:
+            out.append(a + b)
+    return out
+
+
+def class_id(c) -> str:
+    return "%d%d%d%d" % tuple(c)
+
+
+def ncart(L: int) -> int:
+    return (L + 1) * (L + 2) // 2
+
+
+DIRS = "xyz"
+
+
+def _coef_expr(kind: int, d: int, side_swap: bool) -> str:
+    """Symbolic coefficient -> device expression. With side_swap the plan's
+    bra is the kernel's ket (roles of p/q, P/Q exchanged)."""
+    if side_swap:
+        kind = {PA: QC, QC: PA, WP: WQ, WQ: WP, I2P: I2Q, I2Q: I2P, ITP_RP: ITQ_RQ,
+                ITQ_RQ: ITP_RP, AB: CD, CD: AB, PB: QD, QD: PB}.get(kind, kind)
+    x = DIRS[d]
+    return {
+        UNIT: "1.0",
+        PA: f"bPA{x}", QC: f"kPA{x}", WP: f"WP{x}", WQ: f"WQ{x}",
+        I2P: "i2p", I2Q: "i2q", I2PQ: "i2pq", ITP_RP: "itp", ITQ_RQ: "itq",
+        AB: f"AB{x}", CD: f"CD{x}",
+    }[kind]
+
+
+def _fmt_factor(f: float) -> str:
+    if f == int(f):
+        return "%d.0" % int(f)
+    return repr(f)
+
+
+def emit_class(cls) -> Tuple[str, Dict]:
+    la, lb, lc, ld = cls
+    p_fwd = compile_class(cls)
+    p_swp = compile_class((lc, ld, la, lb))
+    swap = p_swp.op_count < p_fwd.op_count
+    plan = p_swp if swap else p_fwd
+    cid = class_id(cls)
+    M = plan.max_m
+    na, nb, nc, nd = map(ncart, cls)
+
+    lines: List[str] = []
+    w = lines.append
+    # names for nodes
+    lower_name = {n: f"r{i}" for i, n in enumerate(plan.lower_order)}
+    bnd_name = {n: f"t{i}" for i, n in enumerate(plan.boundary)}
+    upper_name = {n: f"h{i}" for i, n in enumerate(plan.upper_order)}
+
+    def val_after_contract(n):
+        if n in upper_name:
+            return upper_name[n]
+        return bnd_name[n]
+
+    w(f"// ERI class ({la},{lb},{lc},{ld}); plan orientation "
+      f"{'(ket|bra)' if swap else '(bra|ket)'}; ops {plan.op_count}; "
+      f"boundary {len(plan.boundary)}; max_m {M}")
+    w(f"struct Cls{cid} {{")
+    w(f"  static constexpr int LA = {la}, LB = {lb}, LC = {lc}, LD = {ld};")
+    w(f"  static constexpr int NA = {na}, NB = {nb}, NC = {nc}, ND = {nd};")
+    w(f"  static constexpr int NV = {na * nb * nc * nd};")
+    w(f"  static constexpr int M = {M};")
+    w(f"  static constexpr int OPS = {plan.op_count};")
+    w("  __device__ __forceinline__ static void eri(")
+    w("      const PrimRec* __restrict__ bra, int kb, const PrimRec* __restrict__ ket, int kk,")
+    w("      double ABx, double ABy, double ABz, double CDx, double CDy, double CDz,")
+    w("      const double* __restrict__ btab, double (&out)[NV]) {")
+    for n, t in bnd_name.items():
+        w(f"    double {t} = 0.0;")
+    w("    for (int j = 0; j < kk; ++j) {")
+    w("      const PrimRec kp = load_prim(ket + j);")
+    w("      for (int i = 0; i < kb; ++i) {")
+    w("        const PrimRec bp = load_prim(bra + i);")
+    w("        const double pq = bp.p + kp.p;")
+    w("        const double rs = rsqrt(pq);")
+    w("        const double inv = rs * rs;")
+    w("        const double PQx = bp.Px - kp.Px, PQy = bp.Py - kp.Py, PQz = bp.Pz - kp.Pz;")
+    w("        const double pinv = bp.p * inv, qinv = kp.p * inv;")
+    w("        const double rho = bp.p * qinv;")
+    w("        const double T = rho * fma(PQx, PQx, fma(PQy, PQy, PQz * PQz));")
+    w("        const double pref = bp.U * kp.U * rs;")
+    w(f"        double F[{M + 1}];")
+    w(f"        boys_eval<{M}>(T, btab, F);")
+    if M > 0:
+        w("        const double WPx = -qinv * PQx, WPy = -qinv * PQy, WPz = -qinv * PQz;")
+        w("        const double WQx = pinv * PQx, WQy = pinv * PQy, WQz = pinv * PQz;")
+        w("        const double bPAx = bp.PAx, bPAy = bp.PAy, bPAz = bp.PAz;")
+        w("        const double kPAx = kp.PAx, kPAy = kp.PAy, kPAz = kp.PAz;")
+        w("        const double i2p = bp.i2p, i2q = kp.i2p, i2pq = 0.5 * inv;")
+        w("        const double itp = bp.i2p * qinv, itq = kp.i2p * pinv;")
+        w("        (void)WPx; (void)WPy; (void)WPz; (void)WQx; (void)WQy; (void)WQz;")
+        w("        (void)bPAx; (void)bPAy; (void)bPAz; (void)kPAx; (void)kPAy; (void)kPAz;")
+        w("        (void)i2p; (void)i2q; (void)i2pq; (void)itp; (void)itq;")
+    # primitive segment
+    for n in plan.lower_order:
+        nm = lower_name[n]
+        if is_base(n):
+            w(f"        const double {nm} = pref * F[{n[4]}];")
+            continue
+        terms = plan.deriv[n]
+        expr = None
+        for t in terms:
+            c = _coef_expr(t.kind, t.dir, swap)
+            src = lower_name[t.node]
+            if t.factor != 1.0:
+                c = f"({_fmt_factor(t.factor)} * {c})"
+            expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
+        w(f"        const double {nm} = {expr};")
+    for n in plan.boundary:
+        w(f"        {bnd_name[n]} += {lower_name[n]};")
+    w("      }")
+    w("    }")
+    # contracted segment
+    for n in plan.upper_order:
+        expr = None
+        for t in plan.deriv[n]:
+            c = _coef_expr(t.kind, t.dir, swap)
+            src = val_after_contract(t.node)
+            if t.kind == UNIT and t.factor == 1.0:
+                expr = src if expr is None else f"({expr} + {src})"
+            else:
+                if t.factor != 1.0:
+                    c = f"({_fmt_factor(t.factor)} * {c})"
+                expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
+        w(f"    const double {upper_name[n]} = {expr};")
+    # targets: map kernel a-major (a,b,c,d) -> plan node
+    ca, cb, cc, cd = (components(L) for L in cls)
+    k = 0
+    for a in ca:
+        for b in cb:
+            for c in cc:
+                for d in cd:
+                    node = (c, d, a, b, 0) if swap else (a, b, c, d, 0)
+                    w(f"    out[{k}] = {val_after_contract(node)};")
+                    k += 1
+    w("  }")
+    w("};")
+    info = dict(cls=cls, swap=swap, ops=plan.op_count, M=M, nv=na * nb * nc * nd,
+                boundary=len(plan.boundary), prim_terms=sum(len(i.terms) for i in plan.prim if i.base_m < 0),
+                base=sum(1 for i in plan.prim if i.base_m >= 0), contract=len(plan.contract),
+                hrr_terms=sum(len(i.terms) for i in plan.hrr))
+    return "\n".join(lines) + "\n", info
+
+
+def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
+    outdir.mkdir(parents=True, exist_ok=True)
+    infos = []
+    classes = canonical_classes(lmax)
+    for idx, cls in enumerate(classes):
+        body, info = emit_class(cls)
+        cid = class_id(cls)
+        info["index"] = idx
+        infos.append(info)
+        src = [
+            "// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
+            '#include "../jk_kernels.cuh"',
+            "namespace eritile_b200 {",
+            body,
+            f"void launch_cls{cid}(const LaunchArgs& a) {{ launch_class<Cls{cid}>(a); }}",
+            "}  // namespace eritile_b200",
+            "",
+        ]
+        _write_if_changed(outdir / f"cls_{cid}.cu", "\n".join(src))
+    reg = ["// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
+           '#include "../jk_api.h"', "namespace eritile_b200 {"]
+    for info in infos:
+        reg.append(f"void launch_cls{class_id(info['cls'])}(const LaunchArgs&);")
+    reg.append("const ClassEntry kClassTable[] = {")
+    for info in infos:
+        la, lb, lc, ld = info["cls"]
+        cid = class_id(info["cls"])
+        reg.append(f"  {{{la}, {lb}, {lc}, {ld}, {info['M']}, {info['ops']}, {info['prim_terms']}, "
+                   f"{info['base']}, {info['contract']}, {info['hrr_terms']}, "
+                   f"&launch_cls{cid}}},")
+    reg.append("};")
+    reg.append(f"const int kNumClasses = {len(infos)};")
+    reg.append(f"const int kMaxL = {lmax};")
+    reg.append("}  // namespace eritile_b200")
+    _write_if_changed(outdir / "registry.cpp", "\n".join(reg) + "\n")
+    return infos
+
+
+def _write_if_changed(path: Path, text: str) -> None:
+    if path.exists() and path.read_text() == text:
+        return
+    tmp = path.with_suffix(path.suffix + ".tmp")
+    tmp.write_text(text)
+    os.replace(tmp, path)

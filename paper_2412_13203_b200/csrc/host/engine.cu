@@ -1,0 +1,939 @@
+// eritile_gpu engine: host Block Constructor, screening, work lists, launch
+// orchestration and the C ABI (include/eritile_gpu.h).
+//
+// Host Block Constructor (block.hpp:52-150 restated for the GPU):
+//  * reference pair store: all S(S+1)/2 shell pairs i<=j with the kappa
+//    screen of block.hpp:83-89, ordered by (Li+Lj, Li, Lj, i, j)
+//    (block.hpp:94-101) — gives each pair its reference index `ref`;
+//  * product pairs: the same pairs oriented A = higher-L shell, grouped by
+//    (L_A+L_B, L_A, L_B, K) and, once Schwarz Q is known, sorted by Q
+//    descending inside each group. Surviving kets of a bra are then a prefix
+//    of every ket group, so quartet lists are (bra, ket range) work items;
+//  * work items: one warp per (bra x, <=32 consecutive kets) of one ket
+//    group, class-homogeneous and contraction-homogeneous (Permutation).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/eritile_gpu.h"
+#include "../jk_api.h"
+#include "../jk_kernels.cuh"
+#include "molecule.h"
+#include "onee.h"
+
+namespace eritile_b200 {
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct StateError : std::runtime_error {
+  explicit StateError(const std::string& m) : std::runtime_error(m) {}
+};
+struct ArgError : std::runtime_error {
+  explicit ArgError(const std::string& m) : std::runtime_error(m) {}
+};
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) return;
+    CK(cudaMalloc(&p, sizeof(T) * count));
+    n = count;
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(v.size());
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+// ------------------------------------------------------------ Boys table
+// F_m(T_i) for T_i = i/16 by the convergent series
+// F_m(T) = e^-T sum_k (2T)^k / ((2m+1)(2m+3)...(2m+2k+1)) in long double
+// (all terms positive: no cancellation), stored as F_{M+k}(T_i)/k!, k<8,
+// plus exp(-T_i) per row, for each slice M = 0..kBoysMmax.
+static std::vector<double> make_boys_table() {
+  const int mtop = kBoysMmax + 8;
+  std::vector<long double> F(static_cast<size_t>(kBoysRows) * (mtop + 1));
+  for (int i = 0; i < kBoysRows; ++i) {
+    const long double T = static_cast<long double>(i) / 16.0L;
+    const long double eT = expl(-T);
+    for (int m = 0; m <= mtop; ++m) {
+      long double term = 1.0L / (2 * m + 1), sum = term;
+      for (int k = 0; k < 2000; ++k) {
+        term *= 2.0L * T / (2 * m + 2 * k + 3);
+        sum += term;
+        if (term < 1e-22L * sum) break;
+      }
+      F[static_cast<size_t>(i) * (mtop + 1) + m] = eT * sum;
+    }
+  }
+  std::vector<double> tab(static_cast<size_t>(kBoysMmax + 1) * kBoysRows * kBoysCols);
+  const long double fact[8] = {1, 1, 2, 6, 24, 120, 720, 5040};
+  for (int M = 0; M <= kBoysMmax; ++M)
+    for (int i = 0; i < kBoysRows; ++i) {
+      double* row = tab.data() + (static_cast<size_t>(M) * kBoysRows + i) * kBoysCols;
+      for (int k = 0; k < 8; ++k)
+        row[k] = static_cast<double>(F[static_cast<size_t>(i) * (mtop + 1) + M + k] / fact[k]);
+      row[8] = static_cast<double>(expl(-static_cast<long double>(i) / 16.0L));
+    }
+  return tab;
+}
+
+// ------------------------------------------------------------- kernels
+__global__ void k_prescale(const double* __restrict__ D, const double* __restrict__ s, double* __restrict__ Ds,
+                           int N) {
+  const size_t NN = static_cast<size_t>(N) * N;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < NN;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = e / N, c = e % N;
+    Ds[e] = D[e] * (s[r] * s[c]);
+  }
+}
+
+// true J = s_mu s_nu (Jacc + Jacc^T)/2, true K likewise (Appendix C).
+__global__ void k_finalize(const double* __restrict__ Jacc, const double* __restrict__ Kacc,
+                           const double* __restrict__ s, double* __restrict__ J, double* __restrict__ K,
+                           int N) {
+  const size_t NN = static_cast<size_t>(N) * N;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < NN;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = e / N, c = e % N, t = c * N + r;
+    const double f = 0.5 * (s[r] * s[c]);
+    J[e] = f * (Jacc[e] + Jacc[t]);
+    K[e] = f * (Kacc[e] + Kacc[t]);
+  }
+}
+
+template <int M>
+__device__ void boys_one(double T, const double* tab, double* out) {
+  double F[M + 1];
+  boys_eval<M>(T, tab + static_cast<size_t>(M) * kBoysRows * kBoysCols, F);
+  for (int m = 0; m <= M; ++m) out[m] = F[m];
+}
+
+// Device Boys values for tests (eritile_gpu_boys); table read from global.
+__global__ void k_boys(int m_max, const double* __restrict__ T, int n, const double* __restrict__ tab,
+                       double* __restrict__ F) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* o = F + static_cast<size_t>(i) * (m_max + 1);
+  switch (m_max) {
+    case 0: boys_one<0>(T[i], tab, o); break;
+    case 1: boys_one<1>(T[i], tab, o); break;
+    case 2: boys_one<2>(T[i], tab, o); break;
+    case 3: boys_one<3>(T[i], tab, o); break;
+    case 4: boys_one<4>(T[i], tab, o); break;
+    case 5: boys_one<5>(T[i], tab, o); break;
+    case 6: boys_one<6>(T[i], tab, o); break;
+    case 7: boys_one<7>(T[i], tab, o); break;
+    case 8: boys_one<8>(T[i], tab, o); break;
+    case 9: boys_one<9>(T[i], tab, o); break;
+    case 10: boys_one<10>(T[i], tab, o); break;
+    case 11: boys_one<11>(T[i], tab, o); break;
+    case 12: boys_one<12>(T[i], tab, o); break;
+    case 13: boys_one<13>(T[i], tab, o); break;
+    case 14: boys_one<14>(T[i], tab, o); break;
+    case 15: boys_one<15>(T[i], tab, o); break;
+    default: boys_one<16>(T[i], tab, o); break;
+  }
+}
+
+// ---------------------------------------------------------------- context
+struct Group {
+  int la, lb, K;
+  int first, count;  // product pair ids
+};
+
+struct ClassWork {
+  int cls;  // index into kClassTable
+  long long off, n;
+  long long quartets, prim_quartets;
+};
+
+}  // namespace eritile_b200
+
+using namespace eritile_b200;
+
+struct eritile_gpu {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+
+  std::vector<Atom> atoms;
+  std::vector<ShellData> shells;
+  std::vector<int> bf_off;
+  std::vector<double> bf_scale;
+  int nbf = 0;
+  bool have_mol = false;
+
+  // reference pair store
+  std::vector<int> ref_i, ref_j;
+  // product pairs
+  std::vector<PairMeta> pm;   // product order
+  std::vector<PrimRec> prims;
+  std::vector<int> prod_of_ref;  // ref index -> product id
+  std::vector<int> cls_of_pair;  // canonical pair class index per product pair
+  std::vector<Group> groups;
+  std::vector<double> Q;  // product order
+  bool have_pairs = false, have_q = false, have_lists = false;
+  int rank = 0, nranks = 1;
+  double tau = 0.0;
+
+  std::vector<WorkItem> items;
+  std::vector<ClassWork> work;
+  long long quartets = 0, prim_quartets = 0;
+  double model_flops = 0.0;
+  double last_build_ms = 0.0, last_schwarz_ms = 0.0;
+  int launches_last = 0;
+
+  DevBuf<PairMeta> d_pm;
+  DevBuf<PrimRec> d_prims;
+  DevBuf<double> d_boys, d_scale, d_Q;
+  DevBuf<WorkItem> d_items;
+  DevBuf<int> d_list;
+  DevBuf<double> d_D, d_Ds, d_JK, d_J, d_K;
+
+  ~eritile_gpu() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  int class_index(int la, int lb, int lc, int ld) const {
+    for (int c = 0; c < kNumClasses; ++c)
+      if (kClassTable[c].la == la && kClassTable[c].lb == lb && kClassTable[c].lc == lc &&
+          kClassTable[c].ld == ld)
+        return c;
+    throw ArgError("no generated kernel for class (" + std::to_string(la) + "," + std::to_string(lb) + "," +
+                   std::to_string(lc) + "," + std::to_string(ld) + ")");
+  }
+
+  void set_molecule(std::vector<Atom> a, std::vector<ShellData> s) {
+    for (const auto& sh : s)
+      if (sh.L > kMaxL) throw ArgError("shell angular momentum exceeds compiled classes");
+    if (s.empty()) throw ArgError("build_pairs: no shells");
+    atoms = std::move(a);
+    shells = std::move(s);
+    bf_off.assign(shells.size() + 1, 0);
+    bf_scale.clear();
+    std::vector<std::array<int, 3>> comps;
+    for (size_t i = 0; i < shells.size(); ++i) {
+      bf_off[i + 1] = bf_off[i] + shells[i].nfunc();
+      cart_components(shells[i].L, comps);
+      for (auto& c : comps) bf_scale.push_back(component_scale(c[0], c[1], c[2]));
+    }
+    nbf = bf_off.back();
+    have_mol = true;
+    have_pairs = have_q = have_lists = false;
+    d_scale.upload(bf_scale);
+  }
+
+  // block.hpp:52-103 restated + product orientation and grouping.
+  void build_pairs(double kappa_screen) {
+    if (!have_mol) throw StateError("build_pairs before a molecule was loaded");
+    const int S = static_cast<int>(shells.size());
+    struct Tmp {
+      int i, j, li, lj;
+      std::vector<PrimRec> pr;
+    };
+    std::vector<Tmp> all;
+    all.reserve(static_cast<size_t>(S) * (S + 1) / 2);
+    const double u_const = std::sqrt(2.0) * std::pow(M_PI, 1.25);
+    for (int i = 0; i < S; ++i)
+      for (int j = i; j < S; ++j) {
+        const ShellData& si = shells[i];
+        const ShellData& sj = shells[j];
+        // kappa and the screen use the reference's (i, j) orientation
+        const double ABi[3] = {si.c[0] - sj.c[0], si.c[1] - sj.c[1], si.c[2] - sj.c[2]};
+        const double ab2 = ABi[0] * ABi[0] + ABi[1] * ABi[1] + ABi[2] * ABi[2];
+        const bool swap = sj.L > si.L;  // orient A = higher L
+        const ShellData& A = swap ? sj : si;
+        const ShellData& B = swap ? si : sj;
+        Tmp t{i, j, si.L, sj.L, {}};
+        for (int k = 0; k < si.K(); ++k)
+          for (int l = 0; l < sj.K(); ++l) {
+            const double alpha = si.exps[k], beta = sj.exps[l];
+            const double p = alpha + beta;
+            const double kappa = std::exp(-alpha * beta * ab2 / p);
+            const double coef = si.coefs[k] * sj.coefs[l];
+            if (kappa_screen > 0.0 && std::fabs(coef) * kappa < kappa_screen) continue;
+            const double ea = swap ? beta : alpha, eb = swap ? alpha : beta;
+            PrimRec r;
+            r.p = p;
+            r.Px = (ea * A.c[0] + eb * B.c[0]) / p;
+            r.Py = (ea * A.c[1] + eb * B.c[1]) / p;
+            r.Pz = (ea * A.c[2] + eb * B.c[2]) / p;
+            r.PAx = r.Px - A.c[0];
+            r.PAy = r.Py - A.c[1];
+            r.PAz = r.Pz - A.c[2];
+            r.U = u_const * kappa * coef / p;
+            r.i2p = 0.5 / p;
+            r.pad = 0.0;
+            t.pr.push_back(r);
+          }
+        if (kappa_screen > 0.0 && t.pr.empty()) continue;
+        all.push_back(std::move(t));
+      }
+    // reference order (block.hpp:94-101)
+    std::vector<int> order(all.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+      const Tmp& a = all[x];
+      const Tmp& b = all[y];
+      return std::make_tuple(a.li + a.lj, a.li, a.lj, a.i, a.j) <
+             std::make_tuple(b.li + b.lj, b.li, b.lj, b.i, b.j);
+    });
+    const int np = static_cast<int>(all.size());
+    ref_i.resize(np);
+    ref_j.resize(np);
+    std::vector<int> ref_of_tmp(np);
+    for (int r = 0; r < np; ++r) {
+      ref_i[r] = all[order[r]].i;
+      ref_j[r] = all[order[r]].j;
+      ref_of_tmp[order[r]] = r;
+    }
+    // product grouping: key (LA+LB, LA, LB, K), then reference index
+    std::vector<int> pord(np);
+    std::iota(pord.begin(), pord.end(), 0);
+    auto gkey = [&](int t) {
+      const Tmp& a = all[t];
+      const int LA = std::max(a.li, a.lj), LB = std::min(a.li, a.lj);
+      return std::make_tuple(LA + LB, LA, LB, static_cast<int>(a.pr.size()), ref_of_tmp[t]);
+    };
+    std::sort(pord.begin(), pord.end(), [&](int x, int y) { return gkey(x) < gkey(y); });
+    pm.assign(np, PairMeta{});
+    prims.clear();
+    prod_of_ref.assign(np, -1);
+    groups.clear();
+    cls_of_pair.assign(np, 0);
+    for (int g = 0; g < np; ++g) {
+      const Tmp& t = all[pord[g]];
+      const bool swap = t.lj > t.li;
+      const int a = swap ? t.j : t.i, b = swap ? t.i : t.j;
+      PairMeta m{};
+      m.prim_off = static_cast<int>(prims.size());
+      m.K = static_cast<int>(t.pr.size());
+      m.sha = a;
+      m.shb = b;
+      m.bfa = bf_off[a];
+      m.bfb = bf_off[b];
+      m.ref = ref_of_tmp[pord[g]];
+      m.ABx = shells[a].c[0] - shells[b].c[0];
+      m.ABy = shells[a].c[1] - shells[b].c[1];
+      m.ABz = shells[a].c[2] - shells[b].c[2];
+      pm[g] = m;
+      prod_of_ref[m.ref] = g;
+      prims.insert(prims.end(), t.pr.begin(), t.pr.end());
+      const int LA = shells[a].L, LB = shells[b].L;
+      if (groups.empty() || groups.back().la != LA || groups.back().lb != LB || groups.back().K != m.K)
+        groups.push_back(Group{LA, LB, m.K, g, 0});
+      groups.back().count++;
+    }
+    d_pm.upload(pm);
+    d_prims.upload(prims);
+    have_pairs = true;
+    have_q = have_lists = false;
+  }
+
+  double elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+
+  void schwarz() {
+    if (!have_pairs) throw StateError("schwarz before build_pairs");
+    const int np = static_cast<int>(pm.size());
+    d_Q.alloc(np);
+    std::vector<int> list;
+    CK(cudaEventRecord(ev0, stream));
+    for (int c = 0; c < kNumClasses; ++c) {
+      const ClassEntry& ce = kClassTable[c];
+      if (ce.la != ce.lc || ce.lb != ce.ld) continue;
+      list.clear();
+      for (const Group& g : groups)
+        if (g.la == ce.la && g.lb == ce.lb)
+          for (int x = g.first; x < g.first + g.count; ++x) list.push_back(x);
+      if (list.empty()) continue;
+      DevBuf<int> dl;
+      dl.upload(list);
+      LaunchArgs a{};
+      a.mode = 1;
+      a.pair_list = dl.p;
+      a.npair_list = static_cast<long long>(list.size());
+      a.Qout = d_Q.p;
+      a.pm = d_pm.p;
+      a.prims = d_prims.p;
+      a.boys_tab = d_boys.p;
+      a.stream = stream;
+      a.block = 128;
+      ce.launch(a);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(stream));
+    }
+    CK(cudaEventRecord(ev1, stream));
+    CK(cudaEventSynchronize(ev1));
+    last_schwarz_ms = elapsed(ev0, ev1);
+    Q.resize(np);
+    CK(cudaMemcpy(Q.data(), d_Q.p, sizeof(double) * np, cudaMemcpyDeviceToHost));
+    have_q = true;
+    have_lists = false;
+  }
+
+  void set_q_ref(const double* Qref) {
+    if (!have_pairs) throw StateError("set_schwarz before build_pairs");
+    Q.resize(pm.size());
+    for (size_t r = 0; r < pm.size(); ++r) Q[prod_of_ref[r]] = Qref[r];
+    have_q = true;
+    have_lists = false;
+  }
+
+  // Sort each group by Q descending (ties: reference index), renumber.
+  void sort_groups_by_q() {
+    std::vector<int> perm(pm.size());
+    std::iota(perm.begin(), perm.end(), 0);
+    for (const Group& g : groups)
+      std::sort(perm.begin() + g.first, perm.begin() + g.first + g.count, [&](int x, int y) {
+        if (Q[x] != Q[y]) return Q[x] > Q[y];
+        return pm[x].ref < pm[y].ref;
+      });
+    std::vector<PairMeta> npm(pm.size());
+    std::vector<double> nQ(pm.size());
+    for (size_t g = 0; g < perm.size(); ++g) {
+      npm[g] = pm[perm[g]];
+      nQ[g] = Q[perm[g]];
+      prod_of_ref[npm[g].ref] = static_cast<int>(g);
+    }
+    pm.swap(npm);
+    Q.swap(nQ);
+    d_pm.upload(pm);
+  }
+
+  void set_screening(double t) {
+    if (!have_pairs) throw StateError("set_screening before build_pairs");
+    if (t > 0.0 && !have_q) schwarz();
+    tau = t;
+    if (t > 0.0) sort_groups_by_q();
+    // enumerate group pairs X >= Y, grouped by angular class
+    struct GP {
+      int X, Y, cls;
+      long long cost;
+    };
+    std::vector<GP> gps;
+    for (int X = 0; X < static_cast<int>(groups.size()); ++X)
+      for (int Y = 0; Y <= X; ++Y) {
+        const Group& gx = groups[X];
+        const Group& gy = groups[Y];
+        GP gp{X, Y, class_index(gx.la, gx.lb, gy.la, gy.lb),
+              static_cast<long long>(gx.K) * gy.K};
+        gps.push_back(gp);
+      }
+    std::stable_sort(gps.begin(), gps.end(), [](const GP& a, const GP& b) {
+      if (a.cls != b.cls) return a.cls < b.cls;
+      return a.cost > b.cost;
+    });
+    items.clear();
+    work.clear();
+    quartets = prim_quartets = 0;
+    model_flops = 0.0;
+    long long counter = 0;  // global item counter within class for sharding
+    for (size_t s = 0; s < gps.size();) {
+      const int cls = gps[s].cls;
+      ClassWork cw{cls, static_cast<long long>(items.size()), 0, 0, 0};
+      counter = 0;
+      for (; s < gps.size() && gps[s].cls == cls; ++s) {
+        const Group& gx = groups[gps[s].X];
+        const Group& gy = groups[gps[s].Y];
+        const bool same = gps[s].X == gps[s].Y;
+        for (int r = 0; r < gx.count; ++r) {
+          const int x = gx.first + r;
+          long long n = gy.count;
+          if (t > 0.0) {
+            // survivors: prefix of the Q-descending ket group
+            const double qx = Q[x];
+            int lo = 0, hi = gy.count;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (qx * Q[gy.first + mid] >= t) lo = mid + 1;
+              else hi = mid;
+            }
+            n = lo;
+          }
+          if (same) n = std::min<long long>(n, r + 1);
+          for (long long b = 0; b < n; b += 32, ++counter) {
+            if (counter % nranks != rank) continue;
+            const int cnt = static_cast<int>(std::min<long long>(32, n - b));
+            items.push_back(WorkItem{x, gy.first + static_cast<int>(b), cnt, cls});
+            cw.quartets += cnt;
+            cw.prim_quartets += static_cast<long long>(cnt) * gx.K * gy.K;
+          }
+        }
+      }
+      cw.n = static_cast<long long>(items.size()) - cw.off;
+      if (cw.n > 0) {
+        work.push_back(cw);
+        quartets += cw.quartets;
+        prim_quartets += cw.prim_quartets;
+        const ClassEntry& ce = kClassTable[cls];
+        const double nv = static_cast<double>((ce.la + 1) * (ce.la + 2) / 2 * (ce.lb + 1) * (ce.lb + 2) / 2 *
+                                              (ce.lc + 1) * (ce.lc + 2) / 2 * (ce.ld + 1) * (ce.ld + 2) / 2);
+        model_flops += static_cast<double>(cw.prim_quartets) *
+                           (42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract)) +
+                       static_cast<double>(cw.quartets) * (2.0 * ce.hrr_terms + 12.0 * nv);
+      }
+    }
+    d_items.upload(items);
+    have_lists = true;
+  }
+
+  void ensure_mats() {
+    const size_t NN = static_cast<size_t>(nbf) * nbf;
+    d_Ds.alloc(NN);
+    d_JK.alloc(2 * NN);
+  }
+
+  // Launch every class over D' (pre-scaled, device) into JKacc (zeroed).
+  void launch_all(const double* dDs, double* dJK, cudaStream_t st) {
+    const size_t NN = static_cast<size_t>(nbf) * nbf;
+    CK(cudaMemsetAsync(dJK, 0, sizeof(double) * 2 * NN, st));
+    launches_last = 1;
+    for (const ClassWork& cw : work) {
+      LaunchArgs a{};
+      a.mode = 0;
+      a.items = d_items.p + cw.off;
+      a.nitems = cw.n;
+      a.pm = d_pm.p;
+      a.prims = d_prims.p;
+      a.D = dDs;
+      a.J = dJK;
+      a.K = dJK + NN;
+      a.N = nbf;
+      a.boys_tab = d_boys.p;
+      a.stream = st;
+      a.block = 128;
+      kClassTable[cw.cls].launch(a);
+      CK(cudaGetLastError());
+      ++launches_last;
+    }
+  }
+
+  void prescale(const double* dD, double* dDs, cudaStream_t st) {
+    const size_t NN = static_cast<size_t>(nbf) * nbf;
+    const int grid = static_cast<int>(std::min<size_t>((NN + 255) / 256, 148 * 32));
+    k_prescale<<<std::max(grid, 1), 256, 0, st>>>(dD, d_scale.p, dDs, nbf);
+    CK(cudaGetLastError());
+  }
+
+  void finalize(const double* dJK, double* dJ, double* dK, cudaStream_t st) {
+    const size_t NN = static_cast<size_t>(nbf) * nbf;
+    const int grid = static_cast<int>(std::min<size_t>((NN + 255) / 256, 148 * 32));
+    k_finalize<<<std::max(grid, 1), 256, 0, st>>>(dJK, dJK + NN, d_scale.p, dJ, dK, nbf);
+    CK(cudaGetLastError());
+  }
+
+  void check_ready() {
+    if (!have_lists) throw StateError("build_jk before set_screening");
+  }
+};
+
+// -------------------------------------------------------------- C ABI
+namespace {
+int fail(eritile_gpu* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  return code;
+}
+template <class F>
+int guard(eritile_gpu* c, F&& f) {
+  try {
+    if (c) CK(cudaSetDevice(c->device));
+    f();
+    return ERITILE_OK;
+  } catch (const InputError& e) {
+    return fail(c, ERITILE_ERR_PARSE, e.what());
+  } catch (const CudaError& e) {
+    return fail(c, ERITILE_ERR_CUDA, e.what());
+  } catch (const StateError& e) {
+    return fail(c, ERITILE_ERR_STATE, e.what());
+  } catch (const ArgError& e) {
+    return fail(c, ERITILE_ERR_ARG, e.what());
+  } catch (const std::exception& e) {
+    return fail(c, ERITILE_ERR_ARG, e.what());
+  }
+}
+thread_local std::string g_create_err;
+}  // namespace
+
+extern "C" {
+
+int eritile_gpu_create(int device, eritile_gpu** out) {
+  if (!out) return ERITILE_ERR_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    g_create_err = "no CUDA device (eritile_gpu has no CPU fallback)";
+    return ERITILE_ERR_CUDA;
+  }
+  if (device < 0 || device >= n) {
+    g_create_err = "device index out of range";
+    return ERITILE_ERR_ARG;
+  }
+  auto c = std::make_unique<eritile_gpu>();
+  c->device = device;
+  int rc = guard(c.get(), [&] {
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    c->d_boys.upload(make_boys_table());
+  });
+  if (rc != ERITILE_OK) {
+    g_create_err = c->err;
+    return rc;
+  }
+  *out = c.release();
+  return ERITILE_OK;
+}
+
+void eritile_gpu_destroy(eritile_gpu* ctx) { delete ctx; }
+
+const char* eritile_gpu_last_error(const eritile_gpu* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+int eritile_gpu_load_molecule(eritile_gpu* ctx, const char* xyz_text, const char* basis_text) {
+  if (!ctx || !xyz_text || !basis_text) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    auto atoms = read_xyz(xyz_text);
+    auto tab = read_basis(basis_text);
+    auto sh = attach_basis(atoms, tab);
+    ctx->set_molecule(std::move(atoms), std::move(sh));
+  });
+}
+
+int eritile_gpu_load_shells(eritile_gpu* ctx, int nshell, const int* L, const int* K, const double* center,
+                            const int* atom, const double* exps, const double* coefs, int natoms,
+                            const int* Z, const double* pos) {
+  if (!ctx || nshell <= 0 || !L || !K || !center || !exps || !coefs) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    std::vector<ShellData> sh(nshell);
+    size_t o = 0;
+    for (int s = 0; s < nshell; ++s) {
+      if (K[s] < 1 || L[s] < 0) throw ArgError("invalid shell");
+      sh[s].L = L[s];
+      sh[s].atom = atom ? atom[s] : -1;
+      for (int d = 0; d < 3; ++d) sh[s].c[d] = center[3 * s + d];
+      sh[s].exps.assign(exps + o, exps + o + K[s]);
+      sh[s].coefs.assign(coefs + o, coefs + o + K[s]);
+      o += K[s];
+    }
+    std::vector<Atom> at(natoms > 0 ? natoms : 0);
+    for (int a = 0; a < natoms; ++a) {
+      at[a].Z = Z[a];
+      for (int d = 0; d < 3; ++d) at[a].r[d] = pos[3 * a + d];
+    }
+    ctx->set_molecule(std::move(at), std::move(sh));
+  });
+}
+
+int eritile_gpu_nbf(const eritile_gpu* ctx) { return ctx ? ctx->nbf : 0; }
+int eritile_gpu_shell_info(const eritile_gpu* ctx, int* L, int* K, int* bf_off) {
+  if (!ctx || !L || !K || !bf_off) return ERITILE_ERR_ARG;
+  for (size_t s = 0; s < ctx->shells.size(); ++s) {
+    L[s] = ctx->shells[s].L;
+    K[s] = ctx->shells[s].K();
+    bf_off[s] = ctx->bf_off[s];
+  }
+  return ERITILE_OK;
+}
+int eritile_gpu_nshells(const eritile_gpu* ctx) { return ctx ? static_cast<int>(ctx->shells.size()) : 0; }
+int eritile_gpu_nelectrons(const eritile_gpu* ctx) {
+  int n = 0;
+  if (ctx)
+    for (const Atom& a : ctx->atoms) n += a.Z;
+  return n;
+}
+double eritile_gpu_nuclear_repulsion(const eritile_gpu* ctx) {
+  double e = 0.0;
+  if (!ctx) return e;
+  for (size_t a = 0; a < ctx->atoms.size(); ++a)
+    for (size_t b = a + 1; b < ctx->atoms.size(); ++b) {
+      double d2 = 0.0;
+      for (int k = 0; k < 3; ++k) {
+        const double d = ctx->atoms[a].r[k] - ctx->atoms[b].r[k];
+        d2 += d * d;
+      }
+      e += static_cast<double>(ctx->atoms[a].Z) * ctx->atoms[b].Z / std::sqrt(d2);
+    }
+  return e;
+}
+
+int eritile_gpu_build_pairs(eritile_gpu* ctx, double kappa_screen) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] { ctx->build_pairs(kappa_screen); });
+}
+int eritile_gpu_npairs(const eritile_gpu* ctx) { return ctx ? static_cast<int>(ctx->pm.size()) : 0; }
+int eritile_gpu_pair_shells(const eritile_gpu* ctx, int* i, int* j) {
+  if (!ctx || !i || !j) return ERITILE_ERR_ARG;
+  std::copy(ctx->ref_i.begin(), ctx->ref_i.end(), i);
+  std::copy(ctx->ref_j.begin(), ctx->ref_j.end(), j);
+  return ERITILE_OK;
+}
+
+int eritile_gpu_schwarz(eritile_gpu* ctx, double* Qref) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->have_q) ctx->schwarz();
+    if (Qref)
+      for (size_t r = 0; r < ctx->pm.size(); ++r) Qref[r] = ctx->Q[ctx->prod_of_ref[r]];
+  });
+}
+int eritile_gpu_set_schwarz(eritile_gpu* ctx, const double* Q) {
+  if (!ctx || !Q) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] { ctx->set_q_ref(Q); });
+}
+
+int eritile_gpu_set_shard(eritile_gpu* ctx, int rank, int nranks) {
+  if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, ERITILE_ERR_ARG, "bad shard");
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  ctx->have_lists = false;
+  return ERITILE_OK;
+}
+
+int eritile_gpu_set_screening(eritile_gpu* ctx, double tau) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] { ctx->set_screening(tau); });
+}
+
+long long eritile_gpu_num_quartets(const eritile_gpu* ctx) { return ctx ? ctx->quartets : -1; }
+
+long long eritile_gpu_quartets(const eritile_gpu* ctx, int* xs, int* ys, long long cap) {
+  if (!ctx || !ctx->have_lists) return -1;
+  std::vector<std::pair<int, int>> q;
+  q.reserve(static_cast<size_t>(ctx->quartets));
+  for (const WorkItem& it : ctx->items) {
+    const int rx = ctx->pm[it.bra].ref;
+    for (int l = 0; l < it.kcnt; ++l) {
+      const int ry = ctx->pm[it.kbeg + l].ref;
+      q.emplace_back(std::min(rx, ry), std::max(rx, ry));
+    }
+  }
+  std::sort(q.begin(), q.end());
+  const long long n = static_cast<long long>(q.size());
+  if (xs && ys)
+    for (long long k = 0; k < std::min(n, cap); ++k) {
+      xs[k] = q[k].first;
+      ys[k] = q[k].second;
+    }
+  return n;
+}
+
+int eritile_gpu_build_jk_partial_device(eritile_gpu* ctx, const double* dD, double* dJKacc, void* stream) {
+  if (!ctx || !dD || !dJKacc) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    ctx->check_ready();
+    ctx->ensure_mats();
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    ctx->prescale(dD, ctx->d_Ds.p, st);
+    ctx->launch_all(ctx->d_Ds.p, dJKacc, st);
+    ctx->launches_last += 1;
+  });
+}
+
+int eritile_gpu_finalize_device(eritile_gpu* ctx, const double* dJKacc, double* dJ, double* dK, void* stream) {
+  if (!ctx || !dJKacc || !dJ || !dK) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    ctx->finalize(dJKacc, dJ, dK, st);
+  });
+}
+
+int eritile_gpu_build_jk_device(eritile_gpu* ctx, const double* dD, double* dJ, double* dK, void* stream) {
+  if (!ctx || !dD || !dJ || !dK) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    ctx->check_ready();
+    ctx->ensure_mats();
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    CK(cudaEventRecord(ctx->ev0, st));
+    ctx->prescale(dD, ctx->d_Ds.p, st);
+    ctx->launch_all(ctx->d_Ds.p, ctx->d_JK.p, st);
+    ctx->finalize(ctx->d_JK.p, dJ, dK, st);
+    ctx->launches_last += 2;
+    CK(cudaEventRecord(ctx->ev1, st));
+  });
+}
+
+int eritile_gpu_build_jk(eritile_gpu* ctx, const double* D, double* J, double* K) {
+  if (!ctx || !D || !J || !K) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    ctx->check_ready();
+    ctx->ensure_mats();
+    const size_t NN = static_cast<size_t>(ctx->nbf) * ctx->nbf;
+    ctx->d_D.alloc(NN);
+    ctx->d_J.alloc(NN);
+    ctx->d_K.alloc(NN);
+    cudaStream_t st = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->d_D.p, D, sizeof(double) * NN, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(ctx->ev0, st));
+    ctx->prescale(ctx->d_D.p, ctx->d_Ds.p, st);
+    ctx->launch_all(ctx->d_Ds.p, ctx->d_JK.p, st);
+    ctx->finalize(ctx->d_JK.p, ctx->d_J.p, ctx->d_K.p, st);
+    ctx->launches_last += 2;
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaMemcpyAsync(J, ctx->d_J.p, sizeof(double) * NN, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(K, ctx->d_K.p, sizeof(double) * NN, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->last_build_ms = ctx->elapsed(ctx->ev0, ctx->ev1);
+  });
+}
+
+int eritile_gpu_one_electron(eritile_gpu* ctx, double* S, double* T, double* V) {
+  if (!ctx || !S || !T || !V) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->have_mol) throw StateError("one_electron before a molecule was loaded");
+    one_electron(ctx->shells, ctx->atoms, ctx->bf_off, ctx->bf_scale, S, T, V);
+  });
+}
+
+int eritile_gpu_boys(eritile_gpu* ctx, int m_max, const double* T, int n, double* F) {
+  if (!ctx || !T || !F || n < 0) return ERITILE_ERR_ARG;
+  if (m_max < 0 || m_max > kBoysMmax) return fail(ctx, ERITILE_ERR_DOMAIN, "boys: order out of range");
+  for (int i = 0; i < n; ++i)
+    if (!(T[i] >= 0.0) || !std::isfinite(T[i]))
+      return fail(ctx, ERITILE_ERR_DOMAIN, "boys: argument must be finite and non-negative");
+  return guard(ctx, [&] {
+    DevBuf<double> dT, dF;
+    dT.upload(std::vector<double>(T, T + n));
+    dF.alloc(static_cast<size_t>(n) * (m_max + 1) + 1);
+    k_boys<<<(n + 127) / 128 + 1, 128, 0, ctx->stream>>>(m_max, dT.p, n, ctx->d_boys.p, dF.p);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(F, dF.p, sizeof(double) * n * (m_max + 1), cudaMemcpyDeviceToHost));
+  });
+}
+
+int eritile_gpu_eri_quartet(eritile_gpu* ctx, int x, int y, double* out) {
+  if (!ctx || !out) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    if (!ctx->have_pairs) throw StateError("eri_quartet before build_pairs");
+    const int np = static_cast<int>(ctx->pm.size());
+    if (x < 0 || y < 0 || x >= np || y >= np) throw ArgError("eri_quartet: pair index out of range");
+    const int px = ctx->prod_of_ref[x], py = ctx->prod_of_ref[y];
+    auto key = [&](int p) {
+      const PairMeta& m = ctx->pm[p];
+      const int LA = ctx->shells[m.sha].L, LB = ctx->shells[m.shb].L;
+      return std::make_tuple(LA + LB, LA, LB);
+    };
+    const bool bk_swap = key(px) < key(py);
+    const int pb = bk_swap ? py : px, pk = bk_swap ? px : py;
+    const PairMeta& mb = ctx->pm[pb];
+    const PairMeta& mk = ctx->pm[pk];
+    const int slot_sh[4] = {mb.sha, mb.shb, mk.sha, mk.shb};
+    const int L[4] = {ctx->shells[slot_sh[0]].L, ctx->shells[slot_sh[1]].L, ctx->shells[slot_sh[2]].L,
+                      ctx->shells[slot_sh[3]].L};
+    const int cls = ctx->class_index(L[0], L[1], L[2], L[3]);
+    int nslot[4];
+    for (int s = 0; s < 4; ++s) nslot[s] = (L[s] + 1) * (L[s] + 2) / 2;
+    const int nv = nslot[0] * nslot[1] * nslot[2] * nslot[3];
+    DevBuf<int> dq;
+    dq.upload(std::vector<int>{pb, pk});
+    DevBuf<double> dv;
+    dv.alloc(nv);
+    LaunchArgs a{};
+    a.mode = 2;
+    a.qpairs = dq.p;
+    a.nq = 1;
+    a.qout = dv.p;
+    a.pm = ctx->d_pm.p;
+    a.prims = ctx->d_prims.p;
+    a.boys_tab = ctx->d_boys.p;
+    a.stream = ctx->stream;
+    a.block = 128;
+    kClassTable[cls].launch(a);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<double> v(nv);
+    CK(cudaMemcpy(v.data(), dv.p, sizeof(double) * nv, cudaMemcpyDeviceToHost));
+    // reference positions (i, j | k, l) -> kernel slots
+    const int R[4] = {ctx->ref_i[x], ctx->ref_j[x], ctx->ref_i[y], ctx->ref_j[y]};
+    int slot_of[4];
+    const int bx = bk_swap ? 2 : 0, by = bk_swap ? 0 : 2;  // kernel slot base of x and y
+    slot_of[0] = (slot_sh[bx] == R[0]) ? bx : bx + 1;
+    slot_of[1] = (slot_of[0] == bx) ? bx + 1 : bx;
+    slot_of[2] = (slot_sh[by] == R[2]) ? by : by + 1;
+    slot_of[3] = (slot_of[2] == by) ? by + 1 : by;
+    std::vector<std::array<int, 3>> comps[4];
+    std::vector<double> sc[4];
+    int nr[4];
+    for (int r = 0; r < 4; ++r) {
+      const int Lr = ctx->shells[R[r]].L;
+      cart_components(Lr, comps[r]);
+      nr[r] = static_cast<int>(comps[r].size());
+      for (auto& c : comps[r]) sc[r].push_back(component_scale(c[0], c[1], c[2]));
+    }
+    int stride[4] = {nslot[1] * nslot[2] * nslot[3], nslot[2] * nslot[3], nslot[3], 1};
+    size_t o = 0;
+    int idx[4];
+    for (idx[0] = 0; idx[0] < nr[0]; ++idx[0])
+      for (idx[1] = 0; idx[1] < nr[1]; ++idx[1])
+        for (idx[2] = 0; idx[2] < nr[2]; ++idx[2])
+          for (idx[3] = 0; idx[3] < nr[3]; ++idx[3], ++o) {
+            int k = 0;
+            for (int r = 0; r < 4; ++r) k += idx[r] * stride[slot_of[r]];
+            out[o] = v[k] * (sc[0][idx[0]] * sc[1][idx[1]] * sc[2][idx[2]] * sc[3][idx[3]]);
+          }
+  });
+}
+
+int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out) {
+  if (!ctx || !out) return ERITILE_ERR_ARG;
+  out->nbf = ctx->nbf;
+  out->nshells = static_cast<int>(ctx->shells.size());
+  out->npairs = static_cast<int>(ctx->pm.size());
+  out->nclasses = static_cast<int>(ctx->work.size());
+  out->quartets = ctx->quartets;
+  out->prim_quartets = ctx->prim_quartets;
+  out->work_items = static_cast<long long>(ctx->items.size());
+  out->model_flops = ctx->model_flops;
+  out->last_build_ms = ctx->last_build_ms;
+  out->last_schwarz_ms = ctx->last_schwarz_ms;
+  out->gpu_launches_last_build = ctx->launches_last;
+  return ERITILE_OK;
+}
+
+int eritile_gpu_num_classes(void) { return kNumClasses; }
+int eritile_gpu_class_info(int i, int* o) {
+  if (i < 0 || i >= kNumClasses || !o) return ERITILE_ERR_ARG;
+  const ClassEntry& c = kClassTable[i];
+  const int v[10] = {c.la, c.lb, c.lc, c.ld, c.max_m, c.ops, c.prim_terms, c.base, c.contract, c.hrr_terms};
+  std::memcpy(o, v, sizeof v);
+  return ERITILE_OK;
+}
+
+}  // extern "C"

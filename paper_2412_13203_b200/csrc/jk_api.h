@@ -1,0 +1,71 @@
+// Host-visible types shared by the host library and the generated kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace eritile_b200 {
+
+// One primitive pair of an oriented shell pair (A = first shell, L_A >= L_B).
+// Restates PrimPair (block.hpp:16-24) for the device: p, P, PA as in
+// build_pairs (block.hpp:76-79); U folds the contraction weight D_ik D_jl
+// (block.hpp:82), kappa (block.hpp:81) and the base-case prefactor
+// 2 pi^(5/2) / (p q sqrt(p+q)) as U_ab U_cd / sqrt(p+q):
+// U = sqrt(2) pi^(5/4) kappa coef / p. PB is never read by a plan and is
+// dropped. 80 bytes, 16-byte aligned.
+struct alignas(16) PrimRec {
+  double p, Px, Py, Pz, PAx, PAy, PAz, U, i2p, pad;
+};
+
+// Oriented shell pair (product order). `ref` is the reference pair-store
+// index (block.hpp:94-101) used to export quartet lists.
+struct alignas(16) PairMeta {
+  int prim_off, K, bfa, bfb;
+  int sha, shb, ref, pad;
+  double ABx, ABy, ABz, pad2;
+};
+
+// A warp task: bra pair `bra` against kets kbeg .. kbeg+kcnt-1 (kcnt <= 32)
+// in product pair numbering.
+struct alignas(16) WorkItem {
+  int bra, kbeg, kcnt, cls;
+};
+
+constexpr int kBoysCols = 9;      // F_{M..M+7}(T_i)/k!, exp(-T_i)
+constexpr int kBoysRows = 641;    // T_i = i/16, T < 40
+constexpr double kBoysTmax = 40.0;
+constexpr int kBoysMmax = 16;     // slices M = 0..16 (L <= 4)
+
+struct LaunchArgs {
+  int mode;  // 0 = J/K digestion, 1 = Schwarz diagonal, 2 = raw quartets
+  const WorkItem* items;
+  long long nitems;
+  const int* pair_list;  // Schwarz: product pair ids
+  long long npair_list;
+  double* Qout;          // Schwarz: per product pair
+  const int* qpairs;     // mode 2: (bra, ket) product pair ids
+  long long nq;
+  double* qout;          // mode 2: NV raw values per quartet, kernel order
+  const PairMeta* pm;
+  const PrimRec* prims;
+  const double* D;
+  double* J;
+  double* K;
+  int N;
+  const double* boys_tab;  // kBoysMmax+1 slices of kBoysRows*kBoysCols
+  cudaStream_t stream;
+  int grid;   // 0 = auto
+  int block;  // threads per CTA
+};
+
+using LaunchFn = void (*)(const LaunchArgs&);
+
+struct ClassEntry {
+  int la, lb, lc, ld, max_m, ops, prim_terms, base, contract, hrr_terms;
+  LaunchFn launch;
+};
+
+extern const ClassEntry kClassTable[];
+extern const int kNumClasses;
+extern const int kMaxL;
+
+}  // namespace eritile_b200

@@ -1,0 +1,149 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle.
+
+Bars (BASELINE.json north_star): J/K within 1e-10 absolute, identical
+screened-quartet lists (bit-exact reference pair-store indexing), SCF energy
+within 1e-8 Ha (tests/test_gpu_scf.py).
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import Oracle
+from systems import BASIS, geom
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(xyz, basis, tau):
+    from paper_2412_13203_b200.eritile import Engine
+    e = Engine(0).load_molecule(xyz, basis).build_pairs(0.0)
+    e.set_screening(tau)
+    return e
+
+
+def _rand_density(n, seed=0):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((n, n))
+    return (A + A.T) / np.sqrt(n)
+
+
+def test_boys_device_vs_reference(gpu):
+    from paper_2412_13203_b200.eritile import Engine
+    e = Engine(0)
+    o = Oracle("orc")
+    Ts = np.array([0.0, 1e-6, 1e-3, 0.5, 1.0, 2.03125, 5.0, 12.7, 20.0, 33.3, 35.999, 36.0, 39.99,
+                   40.0, 40.01, 50.0, 79.9, 80.1, 200.0, 1e4])
+    for m in range(0, 17):
+        F = e.boys(m, Ts)
+        for t, row in zip(Ts, F):
+            ref = o.boys(m, float(t))
+            assert np.allclose(row, ref, rtol=2e-14, atol=1e-300), (m, t, row, ref)
+
+
+@pytest.mark.parametrize("mol,basis", [("water", "sto-3g"), ("water", "cc-pvdz"), ("benzene", "6-31g*")])
+def test_eri_quartets_all_classes(gpu, mol, basis):
+    xyz, bas = geom(mol), BASIS[basis]
+    e = _engine(xyz, bas, 0.0)
+    O = Oracle("orc").system(xyz, bas)
+    n = O.npairs
+    rng = np.random.default_rng(1)
+    pairs = [(x, y) for x in range(n) for y in range(x, n)]
+    if len(pairs) > 3000:
+        idx = rng.choice(len(pairs), 3000, replace=False)
+        pairs = [pairs[i] for i in idx]
+    worst = 0.0
+    for x, y in pairs:
+        g = e.eri_quartet(x, y)
+        r = O.eri(x, y)
+        worst = max(worst, float(np.max(np.abs(g - r) / (1.0 + np.abs(r)))))
+        assert np.allclose(g, r, rtol=1e-12, atol=1e-14), (x, y, np.max(np.abs(g - r)))
+    assert worst < 1e-12
+
+
+@pytest.mark.parametrize("mol,basis", [("water", "cc-pvdz"), ("benzene", "6-31g*"), ("w8", "cc-pvdz")])
+def test_schwarz_and_quartet_lists(gpu, mol, basis):
+    xyz, bas = geom(mol), BASIS[basis]
+    e = _engine(xyz, bas, 0.0)
+    O = Oracle("orc").system(xyz, bas)
+    Qg = e.schwarz()
+    Qo = O.schwarz()
+    assert np.allclose(Qg, Qo, rtol=1e-13, atol=1e-300)
+    for tau in (1e-10, 1e-12):
+        e.set_screening(tau)
+        xs, ys = e.quartets()
+        ox, oy = O.quartets(tau)
+        order = np.lexsort((oy, ox))
+        assert len(xs) == len(ox)
+        assert np.array_equal(xs, ox[order]) and np.array_equal(ys, oy[order])
+
+
+def test_quartet_list_shared_q_identity(gpu):
+    """With one shared Q the lists must be identical by construction."""
+    xyz, bas = geom("w4"), BASIS["cc-pvdz"]
+    e = _engine(xyz, bas, 0.0)
+    O = Oracle("orc").system(xyz, bas)
+    Q = O.schwarz()
+    e.set_schwarz(Q)
+    e.set_screening(1e-10)
+    xs, ys = e.quartets()
+    ox, oy = O.quartets(1e-10)
+    order = np.lexsort((oy, ox))
+    assert np.array_equal(xs, ox[order]) and np.array_equal(ys, oy[order])
+
+
+@pytest.mark.parametrize("mol,basis,tau", [("water", "sto-3g", 0.0), ("water", "cc-pvdz", 0.0),
+                                           ("benzene", "6-31g*", 1e-12), ("w4", "cc-pvdz", 1e-10),
+                                           ("w8", "cc-pvdz", 1e-10)])
+def test_jk_vs_oracle(gpu, mol, basis, tau):
+    xyz, bas = geom(mol), BASIS[basis]
+    e = _engine(xyz, bas, tau)
+    O = Oracle("orc").system(xyz, bas)
+    D = _rand_density(e.nbf)
+    J, K = e.build_jk(D)
+    Jo, Ko, nq = O.build_jk(D, tau)
+    assert nq == e.num_quartets()
+    assert np.max(np.abs(J - Jo)) < 1e-10
+    assert np.max(np.abs(K - Ko)) < 1e-10
+    assert np.allclose(J, J.T, atol=1e-14) and np.allclose(K, K.T, atol=1e-14)
+
+
+def test_jk_zero_and_linearity(gpu):
+    xyz, bas = geom("w4"), BASIS["cc-pvdz"]
+    e = _engine(xyz, bas, 1e-10)
+    N = e.nbf
+    J0, K0 = e.build_jk(np.zeros((N, N)))
+    assert not J0.any() and not K0.any()
+    D1, D2 = _rand_density(N, 1), _rand_density(N, 2)
+    J1, K1 = e.build_jk(D1)
+    J2, K2 = e.build_jk(D2)
+    J3, K3 = e.build_jk(0.7 * D1 - 1.3 * D2)
+    assert np.max(np.abs(J3 - (0.7 * J1 - 1.3 * J2))) < 1e-9
+    assert np.max(np.abs(K3 - (0.7 * K1 - 1.3 * K2))) < 1e-9
+
+
+def test_dense_reference_loop_water(gpu):
+    """J/K against a dense O(N^4) einsum over the oracle's full ERI tensor."""
+    xyz, bas = geom("water"), BASIS["sto-3g"]
+    O = Oracle("orc").system(xyz, bas)
+    N = O.nbf
+    sh = O.shells()
+    i, j, _ = O.pairs()
+    nc = lambda l: (l + 1) * (l + 2) // 2
+    G = np.zeros((N, N, N, N))
+    for x in range(O.npairs):
+        for y in range(O.npairs):
+            v = O.eri(x, y)
+            a, b, c, d = i[x], j[x], i[y], j[y]
+            la, lb, lc, ld = (sh["L"][s] for s in (a, b, c, d))
+            v = v.reshape(nc(la), nc(lb), nc(lc), nc(ld))
+            oa, ob, oc, od = (sh["bf_off"][s] for s in (a, b, c, d))
+            blk = G[oa:oa + nc(la), ob:ob + nc(lb), oc:oc + nc(lc), od:od + nc(ld)]
+            blk[...] = v
+            G[ob:ob + nc(lb), oa:oa + nc(la), oc:oc + nc(lc), od:od + nc(ld)] = v.transpose(1, 0, 2, 3)
+            G[oa:oa + nc(la), ob:ob + nc(lb), od:od + nc(ld), oc:oc + nc(lc)] = v.transpose(0, 1, 3, 2)
+            G[ob:ob + nc(lb), oa:oa + nc(la), od:od + nc(ld), oc:oc + nc(lc)] = v.transpose(1, 0, 3, 2)
+    D = _rand_density(N, 5)
+    Jd = np.einsum("mnls,ls->mn", G, D)
+    Kd = np.einsum("mlns,ls->mn", G, D)
+    e = _engine(xyz, bas, 0.0)
+    J, K = e.build_jk(D)
+    assert np.max(np.abs(J - Jd)) < 1e-10 and np.max(np.abs(K - Kd)) < 1e-10
