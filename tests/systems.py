@@ -8,6 +8,6 @@ BASIS = {b: read_fixture("basis", f) for b, f in
 
 
 def geom(name: str) -> str:
-    if name.startswith("w"):
+    if name.startswith("w") and name[1:].isdigit():
         return water_cluster(int(name[1:]))
     return read_fixture("geom", name + ".xyz")
