@@ -117,6 +117,13 @@ int eritile_gpu_boys(eritile_gpu* ctx, int m_max, const double* T, int n, double
 int eritile_gpu_eri_quartet(eritile_gpu* ctx, int x, int y, double* out);
 
 int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out);
+/* Profiling: with on != 0 every class launch is bracketed by CUDA events on
+ * the launch stream. class_profile returns the number of class launches and
+ * fills (up to cap) the class (4 ints), last device time (ms), model FLOPs,
+ * quartets and primitive quartets of each. */
+int eritile_gpu_set_profiling(eritile_gpu* ctx, int on);
+int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, double* flops,
+                              long long* quartets, long long* prim_quartets);
 /* Plan statistics of the generated class kernels, i < num_classes:
  * la lb lc ld max_m ops prim_terms base contract hrr_terms. */
 int eritile_gpu_num_classes(void);

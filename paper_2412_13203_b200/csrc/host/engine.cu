@@ -174,6 +174,8 @@ struct ClassWork {
   int cls;  // index into kClassTable
   long long off, n;
   long long quartets, prim_quartets;
+  double flops = 0.0;    // model FLOPs of this class launch
+  double last_ms = 0.0;  // device time of the last launch (profiling mode)
 };
 
 }  // namespace eritile_b200
@@ -220,7 +222,11 @@ struct eritile_gpu {
   DevBuf<int> d_list;
   DevBuf<double> d_D, d_Ds, d_JK, d_J, d_K;
 
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_ev;
+
   ~eritile_gpu() {
+    for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -466,7 +472,7 @@ struct eritile_gpu {
     long long counter = 0;  // global item counter within class for sharding
     for (size_t s = 0; s < gps.size();) {
       const int cls = gps[s].cls;
-      ClassWork cw{cls, static_cast<long long>(items.size()), 0, 0, 0};
+      ClassWork cw{cls, static_cast<long long>(items.size()), 0, 0, 0, 0.0, 0.0};
       counter = 0;
       for (; s < gps.size() && gps[s].cls == cls; ++s) {
         const Group& gx = groups[gps[s].X];
@@ -498,15 +504,18 @@ struct eritile_gpu {
       }
       cw.n = static_cast<long long>(items.size()) - cw.off;
       if (cw.n > 0) {
-        work.push_back(cw);
-        quartets += cw.quartets;
-        prim_quartets += cw.prim_quartets;
         const ClassEntry& ce = kClassTable[cls];
         const double nv = static_cast<double>((ce.la + 1) * (ce.la + 2) / 2 * (ce.lb + 1) * (ce.lb + 2) / 2 *
                                               (ce.lc + 1) * (ce.lc + 2) / 2 * (ce.ld + 1) * (ce.ld + 2) / 2);
-        model_flops += static_cast<double>(cw.prim_quartets) *
-                           (42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract)) +
-                       static_cast<double>(cw.quartets) * (2.0 * ce.hrr_terms + 12.0 * nv);
+        // F_c = Nprim (42 + 3m + 2(P+B+X)) + Nq (2H + 12 n), with
+        // P, B, X, H from the plan this kernel executes.
+        cw.flops = static_cast<double>(cw.prim_quartets) *
+                       (42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract)) +
+                   static_cast<double>(cw.quartets) * (2.0 * ce.hrr_terms + 12.0 * nv);
+        model_flops += cw.flops;
+        quartets += cw.quartets;
+        prim_quartets += cw.prim_quartets;
+        work.push_back(cw);
       }
     }
     d_items.upload(items);
@@ -524,7 +533,16 @@ struct eritile_gpu {
     const size_t NN = static_cast<size_t>(nbf) * nbf;
     CK(cudaMemsetAsync(dJK, 0, sizeof(double) * 2 * NN, st));
     launches_last = 1;
-    for (const ClassWork& cw : work) {
+    if (profiling && prof_ev.size() < 2 * work.size()) {
+      while (prof_ev.size() < 2 * work.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        prof_ev.push_back(e);
+      }
+    }
+    for (size_t w = 0; w < work.size(); ++w) {
+      const ClassWork& cw = work[w];
+      if (profiling) CK(cudaEventRecord(prof_ev[2 * w], st));
       LaunchArgs a{};
       a.mode = 0;
       a.items = d_items.p + cw.off;
@@ -541,7 +559,15 @@ struct eritile_gpu {
       kClassTable[cw.cls].launch(a);
       CK(cudaGetLastError());
       ++launches_last;
+      if (profiling) CK(cudaEventRecord(prof_ev[2 * w + 1], st));
     }
+  }
+
+  // Per-class device times of the last launch_all (profiling mode).
+  void collect_profile() {
+    if (!profiling) return;
+    CK(cudaEventSynchronize(prof_ev[2 * work.size() - 1]));
+    for (size_t w = 0; w < work.size(); ++w) work[w].last_ms = elapsed(prof_ev[2 * w], prof_ev[2 * w + 1]);
   }
 
   void prescale(const double* dD, double* dDs, cudaStream_t st) {
@@ -909,6 +935,32 @@ int eritile_gpu_eri_quartet(eritile_gpu* ctx, int x, int y, double* out) {
             out[o] = v[k] * (sc[0][idx[0]] * sc[1][idx[1]] * sc[2][idx[2]] * sc[3][idx[3]]);
           }
   });
+}
+
+int eritile_gpu_set_profiling(eritile_gpu* ctx, int on) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  ctx->profiling = on != 0;
+  return ERITILE_OK;
+}
+
+int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, double* flops,
+                              long long* quartets, long long* prim_quartets) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  int rc = guard(ctx, [&] { ctx->collect_profile(); });
+  if (rc != ERITILE_OK) return rc;
+  const int n = static_cast<int>(ctx->work.size());
+  for (int w = 0; w < std::min(n, cap); ++w) {
+    const ClassWork& cw = ctx->work[w];
+    const ClassEntry& ce = kClassTable[cw.cls];
+    if (cls4) {
+      cls4[4 * w] = ce.la; cls4[4 * w + 1] = ce.lb; cls4[4 * w + 2] = ce.lc; cls4[4 * w + 3] = ce.ld;
+    }
+    if (ms) ms[w] = cw.last_ms;
+    if (flops) flops[w] = cw.flops;
+    if (quartets) quartets[w] = cw.quartets;
+    if (prim_quartets) prim_quartets[w] = cw.prim_quartets;
+  }
+  return n;
 }
 
 int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out) {

@@ -78,6 +78,9 @@ def _lib():
         "eritile_gpu_eri_quartet": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _dp]),
         "eritile_gpu_get_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
         "eritile_gpu_num_classes": (C.c_int, []),
+        "eritile_gpu_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+        "eritile_gpu_class_profile": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                C.c_void_p, C.c_void_p]),
         "eritile_gpu_class_info": (C.c_int, [C.c_int, _ip]),
     }
     for name, (res, args) in sig.items():
@@ -261,6 +264,22 @@ class Engine:
         out = np.zeros(n)
         self._check(self._lib.eritile_gpu_eri_quartet(self._h, x, y, out))
         return out
+
+    def set_profiling(self, on: bool = True):
+        self._check(self._lib.eritile_gpu_set_profiling(self._h, int(on)))
+
+    def class_profile(self):
+        """Per-class launch records of the last build (profiling mode)."""
+        n = self._lib.eritile_gpu_class_profile(self._h, 0, None, None, None, None, None)
+        if n < 0:
+            self._check(n)
+        cls = np.zeros(4 * max(n, 1), np.int32)
+        ms, fl = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        q, pq = np.zeros(max(n, 1), np.int64), np.zeros(max(n, 1), np.int64)
+        self._lib.eritile_gpu_class_profile(self._h, n, cls.ctypes.data, ms.ctypes.data, fl.ctypes.data,
+                                            q.ctypes.data, pq.ctypes.data)
+        return [dict(cls=tuple(int(v) for v in cls[4 * i:4 * i + 4]), ms=float(ms[i]), flops=float(fl[i]),
+                     quartets=int(q[i]), prim_quartets=int(pq[i])) for i in range(n)]
 
     def stats(self) -> dict:
         s = Stats()
