@@ -208,7 +208,8 @@ def run_ours(args, rank, nranks, local_rank):
     st = eng.stats()
     Dh = synthetic_density(N, eng.nelectrons // 2)
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # explicit stream: torch events and our kernels share it
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     D = torch.from_numpy(Dh).to(dev)
     JK = torch.empty(2 * N * N, dtype=torch.float64, device=dev)

@@ -115,10 +115,16 @@ def emit_class(cls) -> Tuple[str, Dict]:
     w("      const double* __restrict__ btab, double (&out)[NV]) {")
     for n, t in bnd_name.items():
         w(f"    double {t} = 0.0;")
+    # software pipelining: the next primitive pair is loaded one iteration
+    # ahead (branch-free clamp) so the L1 latency hides behind this one
+    w("    PrimRec kn = load_prim(ket);")
     w("    for (int j = 0; j < kk; ++j) {")
-    w("      const PrimRec kp = load_prim(ket + j);")
+    w("      const PrimRec kp = kn;")
+    w("      kn = load_prim(ket + (j + 1 < kk ? j + 1 : j));")
+    w("      PrimRec bn = load_prim(bra);")
     w("      for (int i = 0; i < kb; ++i) {")
-    w("        const PrimRec bp = load_prim(bra + i);")
+    w("        const PrimRec bp = bn;")
+    w("        bn = load_prim(bra + (i + 1 < kb ? i + 1 : i));")
     w("        const double pq = bp.p + kp.p;")
     w("        const double rs = rsqrt(pq);")
     w("        const double inv = rs * rs;")

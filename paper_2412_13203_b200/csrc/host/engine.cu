@@ -101,6 +101,7 @@ static std::vector<double> make_boys_table() {
       for (int k = 0; k < 8; ++k)
         row[k] = static_cast<double>(F[static_cast<size_t>(i) * (mtop + 1) + M + k] / fact[k]);
       row[8] = static_cast<double>(expl(-static_cast<long double>(i) / 16.0L));
+      row[9] = 0.0;
     }
   return tab;
 }
@@ -209,6 +210,7 @@ struct eritile_gpu {
   double tau = 0.0;
 
   std::vector<WorkItem> items;
+  std::vector<int> cnt;  // survivor counts per (group pair, bra) + sentinel
   std::vector<ClassWork> work;
   long long quartets = 0, prim_quartets = 0;
   double model_flops = 0.0;
@@ -219,6 +221,7 @@ struct eritile_gpu {
   DevBuf<PrimRec> d_prims;
   DevBuf<double> d_boys, d_scale, d_Q;
   DevBuf<WorkItem> d_items;
+  DevBuf<int> d_cnt;
   DevBuf<int> d_list;
   DevBuf<double> d_D, d_Ds, d_JK, d_J, d_K;
 
@@ -467,17 +470,19 @@ struct eritile_gpu {
     });
     items.clear();
     work.clear();
+    cnt.clear();
     quartets = prim_quartets = 0;
     model_flops = 0.0;
-    long long counter = 0;  // global item counter within class for sharding
     for (size_t s = 0; s < gps.size();) {
       const int cls = gps[s].cls;
       ClassWork cw{cls, static_cast<long long>(items.size()), 0, 0, 0, 0.0, 0.0};
-      counter = 0;
+      long long counter = 0;  // warp-task counter within the class (sharding)
       for (; s < gps.size() && gps[s].cls == cls; ++s) {
         const Group& gx = groups[gps[s].X];
         const Group& gy = groups[gps[s].Y];
         const bool same = gps[s].X == gps[s].Y;
+        const int cbase = static_cast<int>(cnt.size());
+        long long total = 0;
         for (int r = 0; r < gx.count; ++r) {
           const int x = gx.first + r;
           long long n = gy.count;
@@ -493,13 +498,25 @@ struct eritile_gpu {
             n = lo;
           }
           if (same) n = std::min<long long>(n, r + 1);
-          for (long long b = 0; b < n; b += 32, ++counter) {
-            if (counter % nranks != rank) continue;
-            const int cnt = static_cast<int>(std::min<long long>(32, n - b));
-            items.push_back(WorkItem{x, gy.first + static_cast<int>(b), cnt, cls});
-            cw.quartets += cnt;
-            cw.prim_quartets += static_cast<long long>(cnt) * gx.K * gy.K;
+          cnt.push_back(static_cast<int>(n));
+          total += n;
+        }
+        cnt.push_back(0);  // sentinel
+        // cut the flat sequence into warp tasks of 32 quartets
+        int r = 0;      // current bra rank within gx
+        long long off = 0;  // offset within bra r's survivors
+        for (long long base = 0; base < total; base += 32, ++counter) {
+          while (r < gx.count && off >= cnt[cbase + r]) {
+            off -= cnt[cbase + r];
+            ++r;
           }
+          const int nq = static_cast<int>(std::min<long long>(32, total - base));
+          if (counter % nranks == rank) {
+            items.push_back(WorkItem{gx.first + r, static_cast<int>(off) | (nq << 24), cbase + r, gy.first});
+            cw.quartets += nq;
+            cw.prim_quartets += static_cast<long long>(nq) * gx.K * gy.K;
+          }
+          off += 32;
         }
       }
       cw.n = static_cast<long long>(items.size()) - cw.off;
@@ -507,7 +524,7 @@ struct eritile_gpu {
         const ClassEntry& ce = kClassTable[cls];
         const double nv = static_cast<double>((ce.la + 1) * (ce.la + 2) / 2 * (ce.lb + 1) * (ce.lb + 2) / 2 *
                                               (ce.lc + 1) * (ce.lc + 2) / 2 * (ce.ld + 1) * (ce.ld + 2) / 2);
-        // SURVEY.md §8d: F_c = Nprim (42 + 3m + 2(P+B+X)) + Nq (2H + 12 n), with
+        // SURVEY.md 8d: F_c = Nprim (42 + 3m + 2(P+B+X)) + Nq (2H + 12 n), with
         // P, B, X, H from the plan this kernel executes.
         cw.flops = static_cast<double>(cw.prim_quartets) *
                        (42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract)) +
@@ -518,6 +535,7 @@ struct eritile_gpu {
         work.push_back(cw);
       }
     }
+    d_cnt.upload(cnt);
     d_items.upload(items);
     have_lists = true;
   }
@@ -547,6 +565,7 @@ struct eritile_gpu {
       a.mode = 0;
       a.items = d_items.p + cw.off;
       a.nitems = cw.n;
+      a.cnt = d_cnt.p;
       a.pm = d_pm.p;
       a.prims = d_prims.p;
       a.D = dDs;
@@ -764,9 +783,15 @@ long long eritile_gpu_quartets(const eritile_gpu* ctx, int* xs, int* ys, long lo
   std::vector<std::pair<int, int>> q;
   q.reserve(static_cast<size_t>(ctx->quartets));
   for (const WorkItem& it : ctx->items) {
-    const int rx = ctx->pm[it.bra].ref;
-    for (int l = 0; l < it.kcnt; ++l) {
-      const int ry = ctx->pm[it.kbeg + l].ref;
+    const int nq = it.r0nq >> 24;
+    for (int l = 0; l < nq; ++l) {
+      int qq = (it.r0nq & 0xffffff) + l, x = it.bra0, c = it.cntp;
+      while (qq >= ctx->cnt[c]) {
+        qq -= ctx->cnt[c];
+        ++x;
+        ++c;
+      }
+      const int rx = ctx->pm[x].ref, ry = ctx->pm[it.yfirst + qq].ref;
       q.emplace_back(std::min(rx, ry), std::max(rx, ry));
     }
   }

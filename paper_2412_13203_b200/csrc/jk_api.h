@@ -24,13 +24,15 @@ struct alignas(16) PairMeta {
   double ABx, ABy, ABz, pad2;
 };
 
-// A warp task: bra pair `bra` against kets kbeg .. kbeg+kcnt-1 (kcnt <= 32)
-// in product pair numbering.
+// A warp task: 32 consecutive quartets of the flat survivor sequence of one
+// (bra group, ket group) pair. Lane l takes quartet r0 + l counted from bra
+// bra0 (whose survivor count is cnt[cntp]); bra x's kets are yfirst ..
+// yfirst + cnt[x] - 1. r0nq = r0 | (nq << 24), nq <= 32 active lanes.
 struct alignas(16) WorkItem {
-  int bra, kbeg, kcnt, cls;
+  int bra0, r0nq, cntp, yfirst;
 };
 
-constexpr int kBoysCols = 9;      // F_{M..M+7}(T_i)/k!, exp(-T_i)
+constexpr int kBoysCols = 10;     // F_{M..M+7}(T_i)/k!, exp(-T_i), pad
 constexpr int kBoysRows = 641;    // T_i = i/16, T < 40
 constexpr double kBoysTmax = 40.0;
 constexpr int kBoysMmax = 16;     // slices M = 0..16 (L <= 4)
@@ -39,6 +41,7 @@ struct LaunchArgs {
   int mode;  // 0 = J/K digestion, 1 = Schwarz diagonal, 2 = raw quartets
   const WorkItem* items;
   long long nitems;
+  const int* cnt;        // survivor counts per (group pair, bra)
   const int* pair_list;  // Schwarz: product pair ids
   long long npair_list;
   double* Qout;          // Schwarz: per product pair

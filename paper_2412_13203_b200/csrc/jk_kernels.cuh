@@ -1,16 +1,19 @@
 // Fused Schwarz-screened ERI + J/K digestion kernels (sm_100a, FP64).
 //
-// Work mapping: one warp per WorkItem = one bra pair x
-// (warp-uniform) against up to 32 ket pairs y (one per lane). Kets of a
-// work item come from one (class, contraction-degree) group sorted by
-// Schwarz Q, so all lanes share the primitive trip count (Permutation).
-// Each lane evaluates its contracted quartet with the class's generated
-// straight-line plan (Cls*::eri), then digests it: J_ab is warp-reduced and
-// flushed once per warp, J_cd and the four K blocks are FP64 atomics
-// (RED.ADD.F64) into the accumulation matrices. The digestion follows the
-// shell-level degeneracy rule of SPEC.md:350 with J weight deg/2 and K
-// weight deg/4, so true J = sym(Jacc) and true K = sym(Kacc) after the
-// finalize kernel.
+// Work mapping: the surviving quartets of one
+// (bra group X, ket group Y) pair are the concatenation, over bras x in X,
+// of a prefix of Y (Y is sorted by Schwarz Q, so survivors of x are the
+// first cnt[x] kets). A warp takes 32 consecutive quartets of that flat
+// sequence (WorkItem = first bra, offset, counts pointer): lanes are kets,
+// runs of lanes share a bra, every lane has the same primitive trip counts
+// (groups are contraction-homogeneous — Permutation). Each
+// lane evaluates its contracted quartet with the class's generated
+// straight-line plan (Cls*::eri), then digests it: J_ab is reduced over the
+// lanes sharing the bra (segmented warp scan) and flushed once per segment;
+// J_cd and the four K blocks are FP64 atomics (RED.ADD.F64). Digestion
+// follows the shell-level degeneracy rule of SPEC.md:350 with J weight
+// deg/2 and K weight deg/4, so true J = sym(Jacc) and K = sym(Kacc) after
+// the finalize kernel.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -29,24 +32,30 @@ __device__ __forceinline__ PrimRec load_prim(const PrimRec* p) {
 
 // Boys function F_0..F_M(T). T < 40: 8-term Taylor expansion of F_M about the
 // nearest grid point T_i = i/16 (|d| <= 1/32, truncation < 3e-17 relative)
-// from a table of F_{M+k}(T_i)/k! computed in extended precision at build
-// time, exp(-T) = exp(-T_i) exp(-d) from the same table, then the stable
-// downward recursion F_{m-1} = (2T F_m + e^-T)/(2m-1) (boys.hpp:40-41).
-// T >= 40: F_0 = sqrt(pi/T)/2 (erf(sqrt T) = 1 - O(1e-19)) and the upward
-// recursion F_{m+1} = ((2m+1) F_m - e^-T)/(2T) (boys.hpp:43), contractive
-// for 2m+1 < 2T; e^-T is dropped above T = 80 where it is < 1e-34.
+// from a table of F_{M+k}(T_i)/k! computed in extended precision when the
+// context is created, exp(-T) = exp(-T_i) exp(-d) from the same table row,
+// then the stable downward recursion F_{m-1} = (2T F_m + e^-T)/(2m-1)
+// (boys.hpp:40-41). T >= 40: F_0 = sqrt(pi/T)/2 (erf(sqrt T) = 1 - O(1e-19))
+// and the upward recursion F_{m+1} = ((2m+1) F_m - e^-T)/(2T) (boys.hpp:43),
+// contractive for 2m+1 < 2T; e^-T is dropped above T = 80 (< 2e-35).
+// Rows are kBoysCols = 10 doubles (16-byte aligned) read as double2.
 template <int M>
 __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ tab, double* F) {
   if (T < kBoysTmax) {
     const int i = __double2int_rn(T * 16.0);
     const double md = fma(static_cast<double>(i), 0.0625, -T);  // -(T - T_i)
-    const double* r = tab + i * kBoysCols;
-    double f = r[7];
-#pragma unroll
-    for (int k = 6; k >= 0; --k) f = fma(f, md, r[k]);
+    const double2* r = reinterpret_cast<const double2*>(tab + i * kBoysCols);
+    const double2 c01 = r[0], c23 = r[1], c45 = r[2], c67 = r[3];
+    double f = fma(c67.y, md, c67.x);
+    f = fma(f, md, c45.y);
+    f = fma(f, md, c45.x);
+    f = fma(f, md, c23.y);
+    f = fma(f, md, c23.x);
+    f = fma(f, md, c01.y);
+    f = fma(f, md, c01.x);
     F[M] = f;
     if (M > 0) {
-      // exp(-d) = sum_k (-d)^k / k!, k <= 8
+      // exp(-d) = sum_k (-d)^k / k!, k <= 8 (|d| <= 1/32)
       double e = 2.48015873015873016e-05;
       e = fma(e, md, 1.98412698412698413e-04);
       e = fma(e, md, 1.38888888888888889e-03);
@@ -56,7 +65,7 @@ __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ t
       e = fma(e, md, 0.5);
       e = fma(e, md, 1.0);
       e = fma(e, md, 1.0);
-      e *= r[8];
+      e *= r[4].x;
       const double T2 = 2.0 * T;
 #pragma unroll
       for (int m = M; m > 0; --m) F[m - 1] = fma(T2, F[m], e) * (1.0 / (2 * m - 1));
@@ -73,15 +82,8 @@ __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ t
   }
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // Component normalisation (molecule.hpp:207-213) for L <= 4, x-major order.
 __device__ __forceinline__ double comp_scale(int L, int i) {
-  // sqrt((2L-1)!! / prod (2a_k-1)!!)
   constexpr double s2[6] = {1.0, 1.7320508075688772, 1.7320508075688772, 1.0, 1.7320508075688772, 1.0};
   constexpr double s3[10] = {1.0, 2.23606797749979, 2.23606797749979, 2.23606797749979,
                              3.872983346207417, 2.23606797749979, 1.0, 2.23606797749979,
@@ -96,32 +98,60 @@ __device__ __forceinline__ double comp_scale(int L, int i) {
   return s4[i];
 }
 
-template <class C>
-__global__ void __launch_bounds__(128) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
-                                                 const PairMeta* __restrict__ pm,
-                                                 const PrimRec* __restrict__ prims,
-                                                 const double* __restrict__ D, double* __restrict__ J,
-                                                 double* __restrict__ K, int N,
-                                                 const double* __restrict__ boys_tab) {
-  extern __shared__ double s_boys[];
-  const double* gt = boys_tab + static_cast<size_t>(C::M) * kBoysRows * kBoysCols;
-  for (int t = threadIdx.x; t < kBoysRows * kBoysCols; t += blockDim.x) s_boys[t] = gt[t];
+// Inclusive segmented sum over lanes with equal non-decreasing key; lanes
+// whose key differs from lane+1 (segment tails) end holding the segment sum.
+__device__ __forceinline__ double seg_sum(double v, int key, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(0xffffffffu, v, o);
+    const int k = __shfl_up_sync(0xffffffffu, key, o);
+    if (lane >= o && k == key) v += u;
+  }
+  return v;
+}
+
+__device__ __forceinline__ void load_boys_slice(double* s_boys, const double* boys_tab, int M) {
+  const double2* gt = reinterpret_cast<const double2*>(boys_tab + static_cast<size_t>(M) * kBoysRows * kBoysCols);
+  double2* st = reinterpret_cast<double2*>(s_boys);
+  for (int t = threadIdx.x; t < kBoysRows * kBoysCols / 2; t += blockDim.x) st[t] = gt[t];
   __syncthreads();
+}
+
+constexpr int kJkThreads = 256;
+
+template <class C>
+__global__ void __launch_bounds__(kJkThreads) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
+                                                       const int* __restrict__ cnt,
+                                                       const PairMeta* __restrict__ pm,
+                                                       const PrimRec* __restrict__ prims,
+                                                       const double* __restrict__ D, double* __restrict__ J,
+                                                       double* __restrict__ K, int N,
+                                                       const double* __restrict__ boys_tab) {
+  extern __shared__ __align__(16) double s_boys[];
+  load_boys_slice(s_boys, boys_tab, C::M);
 
   const int lane = threadIdx.x & 31;
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   for (long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
        w < nitems; w += warps) {
     const WorkItem it = items[w];
-    const PairMeta bm = pm[it.bra];
-    const bool active = lane < it.kcnt;
-    const int y = it.kbeg + (active ? lane : 0);
+    const int nq = it.r0nq >> 24;
+    const bool active = lane < nq;
+    // walk the per-bra survivor counts to this lane's (bra, ket)
+    int q = (it.r0nq & 0xffffff) + (active ? lane : 0);
+    int x = it.bra0, c = it.cntp;
+    for (int n = __ldg(cnt + c); q >= n; n = __ldg(cnt + c)) {
+      q -= n;
+      ++x;
+      ++c;
+    }
+    const int y = it.yfirst + q;
+    const PairMeta bm = pm[x];
     const PairMeta km = pm[y];
     double v[C::NV];
     C::eri(prims + bm.prim_off, bm.K, prims + km.prim_off, active ? km.K : 0, bm.ABx, bm.ABy, bm.ABz,
            km.ABx, km.ABy, km.ABz, s_boys, v);
-    const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) *
-                       (it.bra != y ? 2.0 : 1.0);
+    const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (x != y ? 2.0 : 1.0);
     const double wj = active ? 0.5 * deg : 0.0;
     const double wk = active ? 0.25 * deg : 0.0;
     const size_t n = static_cast<size_t>(N);
@@ -131,23 +161,26 @@ __global__ void __launch_bounds__(128) jk_kernel(const WorkItem* __restrict__ it
     const double* Dad = D + bm.bfa * n + km.bfb;
     const double* Dbc = D + bm.bfb * n + km.bfa;
     const double* Dbd = D + bm.bfb * n + km.bfb;
-    // J_ab: warp-uniform bra -> reduce over lanes, one flush per warp
+    // J_ab: lanes sharing the bra form a segment -> one flush per segment
+    const int xkey = active ? x : -1;
+    const int xnext = __shfl_down_sync(0xffffffffu, xkey, 1);
+    const bool tail = active && (lane == 31 || xnext != xkey);
 #pragma unroll
     for (int a = 0; a < C::NA; ++a)
 #pragma unroll
       for (int b = 0; b < C::NB; ++b) {
         double s = 0.0;
 #pragma unroll
-        for (int c = 0; c < C::NC; ++c)
+        for (int c2 = 0; c2 < C::NC; ++c2)
 #pragma unroll
           for (int d = 0; d < C::ND; ++d)
-            s = fma(v[((a * C::NB + b) * C::NC + c) * C::ND + d], __ldg(Dcd + c * n + d), s);
-        s = warp_sum(s * wj);
-        if (lane == 0) atomicAdd(J + (bm.bfa + a) * n + bm.bfb + b, s);
+            s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dcd + c2 * n + d), s);
+        s = seg_sum(s * wj, xkey, lane);
+        if (tail) atomicAdd(J + (bm.bfa + a) * n + bm.bfb + b, s);
       }
     if (active) {
 #pragma unroll
-      for (int c = 0; c < C::NC; ++c)
+      for (int c2 = 0; c2 < C::NC; ++c2)
 #pragma unroll
         for (int d = 0; d < C::ND; ++d) {
           double s = 0.0;
@@ -155,21 +188,21 @@ __global__ void __launch_bounds__(128) jk_kernel(const WorkItem* __restrict__ it
           for (int a = 0; a < C::NA; ++a)
 #pragma unroll
             for (int b = 0; b < C::NB; ++b)
-              s = fma(v[((a * C::NB + b) * C::NC + c) * C::ND + d], __ldg(Dab + a * n + b), s);
-          atomicAdd(J + (km.bfa + c) * n + km.bfb + d, s * wj);
+              s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dab + a * n + b), s);
+          atomicAdd(J + (km.bfa + c2) * n + km.bfb + d, s * wj);
         }
       // K_ac += sum_bd v D_bd ; K_bd += sum_ac v D_ac
 #pragma unroll
       for (int a = 0; a < C::NA; ++a)
 #pragma unroll
-        for (int c = 0; c < C::NC; ++c) {
+        for (int c2 = 0; c2 < C::NC; ++c2) {
           double s = 0.0;
 #pragma unroll
           for (int b = 0; b < C::NB; ++b)
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
-              s = fma(v[((a * C::NB + b) * C::NC + c) * C::ND + d], __ldg(Dbd + b * n + d), s);
-          atomicAdd(K + (bm.bfa + a) * n + km.bfa + c, s * wk);
+              s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbd + b * n + d), s);
+          atomicAdd(K + (bm.bfa + a) * n + km.bfa + c2, s * wk);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
@@ -179,8 +212,8 @@ __global__ void __launch_bounds__(128) jk_kernel(const WorkItem* __restrict__ it
 #pragma unroll
           for (int a = 0; a < C::NA; ++a)
 #pragma unroll
-            for (int c = 0; c < C::NC; ++c)
-              s = fma(v[((a * C::NB + b) * C::NC + c) * C::ND + d], __ldg(Dac + a * n + c), s);
+            for (int c2 = 0; c2 < C::NC; ++c2)
+              s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dac + a * n + c2), s);
           atomicAdd(K + (bm.bfb + b) * n + km.bfb + d, s * wk);
         }
       // K_ad += sum_bc v D_bc ; K_bc += sum_ad v D_ad
@@ -192,21 +225,21 @@ __global__ void __launch_bounds__(128) jk_kernel(const WorkItem* __restrict__ it
 #pragma unroll
           for (int b = 0; b < C::NB; ++b)
 #pragma unroll
-            for (int c = 0; c < C::NC; ++c)
-              s = fma(v[((a * C::NB + b) * C::NC + c) * C::ND + d], __ldg(Dbc + b * n + c), s);
+            for (int c2 = 0; c2 < C::NC; ++c2)
+              s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbc + b * n + c2), s);
           atomicAdd(K + (bm.bfa + a) * n + km.bfb + d, s * wk);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
 #pragma unroll
-        for (int c = 0; c < C::NC; ++c) {
+        for (int c2 = 0; c2 < C::NC; ++c2) {
           double s = 0.0;
 #pragma unroll
           for (int a = 0; a < C::NA; ++a)
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
-              s = fma(v[((a * C::NB + b) * C::NC + c) * C::ND + d], __ldg(Dad + a * n + d), s);
-          atomicAdd(K + (bm.bfb + b) * n + km.bfa + c, s * wk);
+              s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dad + a * n + d), s);
+          atomicAdd(K + (bm.bfb + b) * n + km.bfa + c2, s * wk);
         }
     }
   }
@@ -220,10 +253,8 @@ __global__ void __launch_bounds__(128) schwarz_kernel(const int* __restrict__ li
                                                       const PrimRec* __restrict__ prims,
                                                       double* __restrict__ Q,
                                                       const double* __restrict__ boys_tab) {
-  extern __shared__ double s_boys[];
-  const double* gt = boys_tab + static_cast<size_t>(C::M) * kBoysRows * kBoysCols;
-  for (int t = threadIdx.x; t < kBoysRows * kBoysCols; t += blockDim.x) s_boys[t] = gt[t];
-  __syncthreads();
+  extern __shared__ __align__(16) double s_boys[];
+  load_boys_slice(s_boys, boys_tab, C::M);
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int x = list[i];
@@ -252,10 +283,8 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
                                                       const PrimRec* __restrict__ prims,
                                                       double* __restrict__ out,
                                                       const double* __restrict__ boys_tab) {
-  extern __shared__ double s_boys[];
-  const double* gt = boys_tab + static_cast<size_t>(C::M) * kBoysRows * kBoysCols;
-  for (int t = threadIdx.x; t < kBoysRows * kBoysCols; t += blockDim.x) s_boys[t] = gt[t];
-  __syncthreads();
+  extern __shared__ __align__(16) double s_boys[];
+  load_boys_slice(s_boys, boys_tab, C::M);
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const PairMeta b = pm[qp[2 * i]], k = pm[qp[2 * i + 1]];
@@ -269,26 +298,35 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 template <class C>
 void launch_class(const LaunchArgs& a) {
   const size_t smem = sizeof(double) * kBoysRows * kBoysCols;
-  const int block = a.block > 0 ? a.block : 128;
   if (a.mode == 0) {
     if (a.nitems <= 0) return;
-    cudaFuncSetAttribute(jk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    long long want = (a.nitems + (block / 32) - 1) / (block / 32);
-    int grid = a.grid > 0 ? a.grid : static_cast<int>(want < 148LL * 16 ? want : 148LL * 16);
-    jk_kernel<C><<<grid, block, smem, a.stream>>>(a.items, a.nitems, a.pm, a.prims, a.D, a.J, a.K,
-                                                  a.N, a.boys_tab);
+    static int blocks_per_sm = 0;
+    static int sms = 0;
+    if (!blocks_per_sm) {
+      cudaFuncSetAttribute(jk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C>, kJkThreads, smem);
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const long long want = (a.nitems + (kJkThreads / 32) - 1) / (kJkThreads / 32);
+    const long long cap = static_cast<long long>(blocks_per_sm) * sms;
+    const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
+    jk_kernel<C><<<grid, kJkThreads, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
+                                                       a.K, a.N, a.boys_tab);
   } else if (a.mode == 2) {
     if (a.nq <= 0) return;
     cudaFuncSetAttribute(quartet_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const int grid = static_cast<int>((a.nq + block - 1) / block);
-    quartet_kernel<C><<<grid, block, smem, a.stream>>>(a.qpairs, a.nq, a.pm, a.prims, a.qout, a.boys_tab);
+    const int grid = static_cast<int>((a.nq + 127) / 128);
+    quartet_kernel<C><<<grid, 128, smem, a.stream>>>(a.qpairs, a.nq, a.pm, a.prims, a.qout, a.boys_tab);
   } else {
     if (a.npair_list <= 0) return;
     cudaFuncSetAttribute(schwarz_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    long long want = (a.npair_list + block - 1) / block;
+    long long want = (a.npair_list + 127) / 128;
     int grid = static_cast<int>(want < 148LL * 16 ? want : 148LL * 16);
-    schwarz_kernel<C><<<grid, block, smem, a.stream>>>(a.pair_list, a.npair_list, a.pm, a.prims,
-                                                       a.Qout, a.boys_tab);
+    schwarz_kernel<C><<<grid, 128, smem, a.stream>>>(a.pair_list, a.npair_list, a.pm, a.prims, a.Qout,
+                                                     a.boys_tab);
   }
 }
 

@@ -1,0 +1,31 @@
+"""Run a few Fock builds of one system (for ncu / nsys-less profiling).
+
+  python tools/profile_build.py --waters 16 --builds 3
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from paper_2412_13203_b200.eritile import Engine, read_fixture  # noqa: E402
+from paper_2412_13203_b200.geometry import water_cluster  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--waters", type=int, default=16)
+ap.add_argument("--basis", default="cc-pvdz.txt")
+ap.add_argument("--tau", type=float, default=1e-10)
+ap.add_argument("--builds", type=int, default=2)
+a = ap.parse_args()
+e = Engine(0).load_molecule(water_cluster(a.waters), read_fixture("basis", a.basis)).build_pairs(0.0)
+e.set_screening(a.tau)
+N = e.nbf
+rng = np.random.default_rng(0)
+C, _ = np.linalg.qr(rng.standard_normal((N, e.nelectrons // 2)))
+D = C @ C.T
+for _ in range(a.builds):
+    J, K = e.build_jk(D)
+print(e.stats())
