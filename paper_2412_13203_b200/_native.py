@@ -9,7 +9,9 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
-LIB = Path(__file__).resolve().parent / "_lib" / "liberitile_b200.so"
+import os
+
+LIB = Path(__file__).resolve().parent / "_lib" / os.environ.get("ERITILE_LIBNAME", "liberitile_b200.so")
 _handle = None
 
 

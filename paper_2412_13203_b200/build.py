@@ -25,14 +25,15 @@ CSRC = PKG / "csrc"
 GEN = CSRC / "generated"
 OBJ = PKG / "_build"
 LIBDIR = PKG / "_lib"
-LIB = LIBDIR / "liberitile_b200.so"
+LIB = LIBDIR / os.environ.get("ERITILE_LIBNAME", "liberitile_b200.so")
 ROOT = PKG.parent
 INCLUDE = ROOT / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
-                  "-I" + str(INCLUDE), "-I" + str(CSRC)]
+                  "-I" + str(INCLUDE), "-I" + str(CSRC),
+                  "-DERITILE_JK_MINB=" + os.environ.get("ERITILE_JK_MINB", "2")]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread", "-I" + str(INCLUDE),
             "-I" + str(CSRC), "-I/usr/local/cuda/include"]
 LMAX = int(os.environ.get("ERITILE_LMAX", "2"))
@@ -50,8 +51,6 @@ def _compile(src: Path, deps, flags, tool) -> Path:
     obj = OBJ / f"{src.stem}.{key}.o"
     if obj.exists():
         return obj
-    for old in OBJ.glob(f"{src.stem}.*.o"):
-        old.unlink()
     tmp = obj.with_suffix(".tmp.o")
     cmd = [tool, *flags, "-c", str(src), "-o", str(tmp)]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -87,7 +86,7 @@ def build(jobs: int | None = None, verbose: bool = True) -> Path:
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(lambda u: _compile(*u), units))
     key = _digest(objs, "link")
-    stamp = LIBDIR / ".link"
+    stamp = LIBDIR / (".link." + LIB.name)
     if LIB.exists() and stamp.exists() and stamp.read_text() == key:
         return LIB
     tmp = LIBDIR / "liberitile_b200.tmp.so"

@@ -55,6 +55,9 @@ def ncart(L: int) -> int:
 
 
 DIRS = "xyz"
+# classes with at most this many plan operations get the two-register
+# ping-pong primitive loop (body emitted twice); larger ones a plain loop
+PINGPONG_MAX_OPS = int(os.environ.get("ERITILE_PINGPONG", "600"))
 
 
 def _coef_expr(kind: int, d: int, side_swap: bool) -> str:
@@ -115,54 +118,78 @@ def emit_class(cls) -> Tuple[str, Dict]:
     w("      const double* __restrict__ btab, double (&out)[NV]) {")
     for n, t in bnd_name.items():
         w(f"    double {t} = 0.0;")
-    # software pipelining: the next primitive pair is loaded one iteration
-    # ahead (branch-free clamp) so the L1 latency hides behind this one
-    w("    PrimRec kn = load_prim(ket);")
-    w("    for (int j = 0; j < kk; ++j) {")
-    w("      const PrimRec kp = kn;")
-    w("      kn = load_prim(ket + (j + 1 < kk ? j + 1 : j));")
-    w("      PrimRec bn = load_prim(bra);")
-    w("      for (int i = 0; i < kb; ++i) {")
-    w("        const PrimRec bp = bn;")
-    w("        bn = load_prim(bra + (i + 1 < kb ? i + 1 : i));")
-    w("        const double pq = bp.p + kp.p;")
-    w("        const double rs = rsqrt(pq);")
-    w("        const double inv = rs * rs;")
-    w("        const double PQx = bp.Px - kp.Px, PQy = bp.Py - kp.Py, PQz = bp.Pz - kp.Pz;")
-    w("        const double pinv = bp.p * inv, qinv = kp.p * inv;")
-    w("        const double rho = bp.p * qinv;")
-    w("        const double T = rho * fma(PQx, PQx, fma(PQy, PQy, PQz * PQz));")
-    w("        const double pref = bp.U * kp.U * rs;")
-    w(f"        double F[{M + 1}];")
-    w(f"        boys_eval<{M}>(T, btab, F);")
+    # Per-primitive-quartet body: binding, Boys, the plan's
+    # primitive segment, fold into the contracted accumulators.
+    body: List[str] = []
+    b = body.append
+    b("const double pq = bp.p + kp.p;")
+    b("const double rs = rsqrt_pos(pq);")
+    b("const double inv = rs * rs;")
+    b("const double PQx = bp.Px - kp.Px, PQy = bp.Py - kp.Py, PQz = bp.Pz - kp.Pz;")
+    b("const double pinv = bp.p * inv, qinv = kp.p * inv;")
+    b("const double rho = bp.p * qinv;")
+    b("const double T = rho * fma(PQx, PQx, fma(PQy, PQy, PQz * PQz));")
+    b("const double pref = bp.U * kp.U * rs;")
+    b(f"double F[{M + 1}];")
+    b(f"boys_eval<{M}>(T, btab, F);")
     if M > 0:
-        w("        const double WPx = -qinv * PQx, WPy = -qinv * PQy, WPz = -qinv * PQz;")
-        w("        const double WQx = pinv * PQx, WQy = pinv * PQy, WQz = pinv * PQz;")
-        w("        const double bPAx = bp.PAx, bPAy = bp.PAy, bPAz = bp.PAz;")
-        w("        const double kPAx = kp.PAx, kPAy = kp.PAy, kPAz = kp.PAz;")
-        w("        const double i2p = bp.i2p, i2q = kp.i2p, i2pq = 0.5 * inv;")
-        w("        const double itp = bp.i2p * qinv, itq = kp.i2p * pinv;")
-        w("        (void)WPx; (void)WPy; (void)WPz; (void)WQx; (void)WQy; (void)WQz;")
-        w("        (void)bPAx; (void)bPAy; (void)bPAz; (void)kPAx; (void)kPAy; (void)kPAz;")
-        w("        (void)i2p; (void)i2q; (void)i2pq; (void)itp; (void)itq;")
-    # primitive segment
+        b("const double WPx = -qinv * PQx, WPy = -qinv * PQy, WPz = -qinv * PQz;")
+        b("const double WQx = pinv * PQx, WQy = pinv * PQy, WQz = pinv * PQz;")
+        b("const double bPAx = bp.PAx, bPAy = bp.PAy, bPAz = bp.PAz;")
+        b("const double kPAx = kp.PAx, kPAy = kp.PAy, kPAz = kp.PAz;")
+        b("const double i2p = bp.i2p, i2q = kp.i2p, i2pq = 0.5 * inv;")
+        b("const double itp = bp.i2p * qinv, itq = kp.i2p * pinv;")
+        b("(void)WPx; (void)WPy; (void)WPz; (void)WQx; (void)WQy; (void)WQz;")
+        b("(void)bPAx; (void)bPAy; (void)bPAz; (void)kPAx; (void)kPAy; (void)kPAz;")
+        b("(void)i2p; (void)i2q; (void)i2pq; (void)itp; (void)itq;")
     for n in plan.lower_order:
         nm = lower_name[n]
         if is_base(n):
-            w(f"        const double {nm} = pref * F[{n[4]}];")
+            b(f"const double {nm} = pref * F[{n[4]}];")
             continue
-        terms = plan.deriv[n]
         expr = None
-        for t in terms:
+        for t in plan.deriv[n]:
             c = _coef_expr(t.kind, t.dir, swap)
             src = lower_name[t.node]
             if t.factor != 1.0:
                 c = f"({_fmt_factor(t.factor)} * {c})"
             expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
-        w(f"        const double {nm} = {expr};")
+        b(f"const double {nm} = {expr};")
     for n in plan.boundary:
-        w(f"        {bnd_name[n]} += {lower_name[n]};")
-    w("      }")
+        b(f"{bnd_name[n]} += {lower_name[n]};")
+
+    def emit_body(var: str, indent: str):
+        w(indent + "{")
+        w(indent + f"  const PrimRec& bp = {var};")
+        for ln in body:
+            w(indent + "  " + ln)
+        w(indent + "}")
+
+    pingpong = plan.op_count <= PINGPONG_MAX_OPS
+    btext = "\n".join(body)
+    bload = "load_prim<%s>" % ("true" if "bPA" in btext else "false")
+    kload = "load_prim<%s>" % ("true" if "kPA" in btext else "false")
+    w("    for (int j = 0; j < kk; ++j) {")
+    w(f"      const PrimRec kp = {kload}(ket + j);")
+    if pingpong:
+        # software pipelining without register copies: two primitive-pair
+        # registers b0/b1 alternate, each reloaded (clamped, branch-free)
+        # right after its last use, so L1 latency hides behind a full body
+        w(f"      PrimRec b0 = {bload}(bra);")
+        w(f"      PrimRec b1 = {bload}(bra + (kb > 1 ? 1 : 0));")
+        w("      for (int i = 0; i < kb; i += 2) {")
+        emit_body("b0", "        ")
+        w(f"        b0 = {bload}(bra + (i + 2 < kb ? i + 2 : kb - 1));")
+        w("        if (i + 1 < kb) {")
+        emit_body("b1", "          ")
+        w("        }")
+        w(f"        b1 = {bload}(bra + (i + 3 < kb ? i + 3 : kb - 1));")
+        w("      }")
+    else:
+        w("      for (int i = 0; i < kb; ++i) {")
+        w(f"        const PrimRec bq = {bload}(bra + i);")
+        emit_body("bq", "        ")
+        w("      }")
     w("    }")
     # contracted segment
     for n in plan.upper_order:

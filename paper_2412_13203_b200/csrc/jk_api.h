@@ -11,9 +11,11 @@ namespace eritile_b200 {
 // (block.hpp:82), kappa (block.hpp:81) and the base-case prefactor
 // 2 pi^(5/2) / (p q sqrt(p+q)) as U_ab U_cd / sqrt(p+q):
 // U = sqrt(2) pi^(5/4) kappa coef / p. PB is never read by a plan and is
-// dropped. 80 bytes, 16-byte aligned.
+// dropped. 80 bytes, 16-byte aligned; the first 48 bytes
+// (p, U, P, 1/2p) are what every class reads, PA follows so classes whose
+// plan never reads PA (QC) on that side skip two 16-byte loads.
 struct alignas(16) PrimRec {
-  double p, Px, Py, Pz, PAx, PAy, PAz, U, i2p, pad;
+  double p, U, Px, Py, Pz, i2p, PAx, PAy, PAz, pad;
 };
 
 // Oriented shell pair (product order). `ref` is the reference pair-store

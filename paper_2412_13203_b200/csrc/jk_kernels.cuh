@@ -21,30 +21,78 @@
 
 namespace eritile_b200 {
 
+#ifndef ERITILE_JK_MINB
+#define ERITILE_JK_MINB 2
+#endif
+
+// Primitive-pair record loads (read-only path). WithPA = false skips the
+// PA/QC half for plans that never read it on that side.
+template <bool WithPA = true>
 __device__ __forceinline__ PrimRec load_prim(const PrimRec* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
-  double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3), e = __ldg(q + 4);
+  const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
   PrimRec r;
-  r.p = a.x; r.Px = a.y; r.Py = b.x; r.Pz = b.y; r.PAx = c.x; r.PAy = c.y; r.PAz = d.x;
-  r.U = d.y; r.i2p = e.x; r.pad = e.y;
+  r.p = a.x; r.U = a.y; r.Px = b.x; r.Py = b.y; r.Pz = c.x; r.i2p = c.y;
+  if (WithPA) {
+    const double2 d = __ldg(q + 3), e = __ldg(q + 4);
+    r.PAx = d.x; r.PAy = d.y; r.PAz = e.x;
+  } else {
+    r.PAx = r.PAy = r.PAz = 0.0;
+  }
+  r.pad = 0.0;
   return r;
 }
 
-// Boys function F_0..F_M(T). T < 40: 8-term Taylor expansion of F_M about the
-// nearest grid point T_i = i/16 (|d| <= 1/32, truncation < 3e-17 relative)
-// from a table of F_{M+k}(T_i)/k! computed in extended precision when the
-// context is created, exp(-T) = exp(-T_i) exp(-d) from the same table row,
-// then the stable downward recursion F_{m-1} = (2T F_m + e^-T)/(2m-1)
+// 1/sqrt(x) for positive normal x: MUFU seed (rsqrt.approx.f64) and one
+// third-order Newton step y' = y + y e (1/2 + 3/8 e), e = 1 - x y^2
+// (seed error ~2^-23 -> < 1 ulp); no special-case branch (inputs are
+// exponent sums and T > 0 here).
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y * y, 1.0);
+  return fma(fma(e, 0.375, 0.5), y * e, y);
+}
+
+// Boys function F_0..F_M(T) (boys.hpp:23-44 semantics, table-driven).
+// T < 40: 8-term Taylor expansion of F_M about the nearest grid point
+// T_i = i/16 (|d| <= 1/32, truncation < 3e-17 relative) from a table of
+// F_{M+k}(T_i)/k! computed in extended precision when the context is
+// created, then the stable downward recursion F_{m-1} = (2T F_m + e^-T)/(2m-1)
 // (boys.hpp:40-41). T >= 40: F_0 = sqrt(pi/T)/2 (erf(sqrt T) = 1 - O(1e-19))
 // and the upward recursion F_{m+1} = ((2m+1) F_m - e^-T)/(2T) (boys.hpp:43),
-// contractive for 2m+1 < 2T; e^-T is dropped above T = 80 (< 2e-35).
-// Rows are kBoysCols = 10 doubles (16-byte aligned) read as double2.
+// contractive for 2m+1 < 2T. e^-T = e^-T_i e^-d uses the table's exp column
+// (for 40 <= T < 80 shifted by e^-40; 0 above 80, < 2e-35), so both branches
+// share one short polynomial. Rows are kBoysCols = 10 doubles, 16-byte
+// aligned, read as double2.
 template <int M>
 __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ tab, double* F) {
-  if (T < kBoysTmax) {
-    const int i = __double2int_rn(T * 16.0);
-    const double md = fma(static_cast<double>(i), 0.0625, -T);  // -(T - T_i)
-    const double2* r = reinterpret_cast<const double2*>(tab + i * kBoysCols);
+  const bool small = T < kBoysTmax;
+  double e = 0.0;
+  const double* row;
+  double md;
+  {
+    const double Tt = small ? T : (T < 2.0 * kBoysTmax ? T - kBoysTmax : 0.0);
+    const int i = __double2int_rn(Tt * 16.0);
+    md = fma(static_cast<double>(i), 0.0625, -Tt);  // -(Tt - T_i)
+    row = tab + i * kBoysCols;
+    if (M > 0) {
+      // exp(-d) = sum_k (-d)^k / k!, k <= 8 (|d| <= 1/32)
+      e = 2.48015873015873016e-05;
+      e = fma(e, md, 1.98412698412698413e-04);
+      e = fma(e, md, 1.38888888888888889e-03);
+      e = fma(e, md, 8.33333333333333333e-03);
+      e = fma(e, md, 4.16666666666666667e-02);
+      e = fma(e, md, 1.66666666666666667e-01);
+      e = fma(e, md, 0.5);
+      e = fma(e, md, 1.0);
+      e = fma(e, md, 1.0);
+      const double scale = small ? 1.0 : (T < 2.0 * kBoysTmax ? 4.24835425529158899e-18 : 0.0);  // e^-40
+      e *= row[8] * scale;
+    }
+  }
+  if (small) {
+    const double2* r = reinterpret_cast<const double2*>(row);
     const double2 c01 = r[0], c23 = r[1], c45 = r[2], c67 = r[3];
     double f = fma(c67.y, md, c67.x);
     f = fma(f, md, c45.y);
@@ -54,27 +102,13 @@ __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ t
     f = fma(f, md, c01.y);
     f = fma(f, md, c01.x);
     F[M] = f;
-    if (M > 0) {
-      // exp(-d) = sum_k (-d)^k / k!, k <= 8 (|d| <= 1/32)
-      double e = 2.48015873015873016e-05;
-      e = fma(e, md, 1.98412698412698413e-04);
-      e = fma(e, md, 1.38888888888888889e-03);
-      e = fma(e, md, 8.33333333333333333e-03);
-      e = fma(e, md, 4.16666666666666667e-02);
-      e = fma(e, md, 1.66666666666666667e-01);
-      e = fma(e, md, 0.5);
-      e = fma(e, md, 1.0);
-      e = fma(e, md, 1.0);
-      e *= r[4].x;
-      const double T2 = 2.0 * T;
+    const double T2 = 2.0 * T;
 #pragma unroll
-      for (int m = M; m > 0; --m) F[m - 1] = fma(T2, F[m], e) * (1.0 / (2 * m - 1));
-    }
+    for (int m = M; m > 0; --m) F[m - 1] = fma(T2, F[m], e) * (1.0 / (2 * m - 1));
   } else {
-    const double rt = rsqrt(T);
+    const double rt = rsqrt_pos(T);
     F[0] = 0.88622692545275801365 * rt;  // sqrt(pi)/2
     if (M > 0) {
-      const double e = T < 80.0 ? exp(-T) : 0.0;
       const double h = 0.5 * rt * rt;  // 1/(2T)
 #pragma unroll
       for (int m = 0; m < M; ++m) F[m + 1] = fma(static_cast<double>(2 * m + 1), F[m], -e) * h;
@@ -120,7 +154,7 @@ __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* bo
 constexpr int kJkThreads = 256;
 
 template <class C>
-__global__ void __launch_bounds__(kJkThreads) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
+__global__ void __launch_bounds__(kJkThreads, ERITILE_JK_MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
                                                        const PairMeta* __restrict__ pm,
                                                        const PrimRec* __restrict__ prims,
