@@ -57,7 +57,10 @@ def ncart(L: int) -> int:
 DIRS = "xyz"
 # classes with at most this many plan operations get the two-register
 # ping-pong primitive loop (body emitted twice); larger ones a plain loop
-PINGPONG_MAX_OPS = int(os.environ.get("ERITILE_PINGPONG", "600"))
+PINGPONG_MAX_OPS = int(os.environ.get("ERITILE_PINGPONG", "0"))
+# single-register prefetch of the next bra primitive pair (measured best,
+# profiles/r01_variants.txt)
+PREFETCH = os.environ.get("ERITILE_PREFETCH", "1") == "1"
 
 
 def _coef_expr(kind: int, d: int, side_swap: bool) -> str:
@@ -184,6 +187,13 @@ def emit_class(cls) -> Tuple[str, Dict]:
         emit_body("b1", "          ")
         w("        }")
         w(f"        b1 = {bload}(bra + (i + 3 < kb ? i + 3 : kb - 1));")
+        w("      }")
+    elif PREFETCH:
+        w(f"      PrimRec bn = {bload}(bra);")
+        w("      for (int i = 0; i < kb; ++i) {")
+        w("        const PrimRec bq = bn;")
+        w(f"        bn = {bload}(bra + (i + 1 < kb ? i + 1 : i));")
+        emit_body("bq", "        ")
         w("      }")
     else:
         w("      for (int i = 0; i < kb; ++i) {")
