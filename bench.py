@@ -163,9 +163,8 @@ def cpu_sample(args, steps: int, warmup: int, target_s: float, reference_arm: bo
     # calibrate: a tiny systematic sample
     stride = max(1, nblocks // 200)
     for _ in range(3):  # calibrate the systematic sample to ~target_s
-        t0 = time.perf_counter()
-        _, _, nq = S.build_jk(D, args.tau, cores, stride, 0)
-        dt = max(time.perf_counter() - t0, 1e-3)
+        _, _, nq, dt = S.build_jk_timed(D, args.tau, cores, stride, 0)
+        dt = max(dt, 1e-3)
         if dt > 0.2 * target_s or stride == 1:
             break
         stride = max(1, int(stride * dt / (0.3 * target_s)))
@@ -174,9 +173,7 @@ def cpu_sample(args, steps: int, warmup: int, target_s: float, reference_arm: bo
     per_step = max(1, min(per_step, nblocks))
     vals, qs, ts = [], 0, 0.0
     for s in range(warmup + steps):
-        t0 = time.perf_counter()
-        _, _, nq = S.build_jk(D, args.tau, cores, per_step, (s * 7919) % per_step)
-        dt = time.perf_counter() - t0
+        _, _, nq, dt = S.build_jk_timed(D, args.tau, cores, per_step, (s * 7919) % per_step)
         if s >= warmup:
             vals.append(nq / dt)
             qs += nq
@@ -184,8 +181,9 @@ def cpu_sample(args, steps: int, warmup: int, target_s: float, reference_arm: bo
     value = qs / ts if ts > 0 else rate
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"every {per_step}-th of {nblocks} QuadBlocks (M=32) per step, {steps} steps, "
-                      f"{qs} quartets in {ts:.1f} s; Schwarz diagonal {tq:.1f} s excluded",
-            "s_per_build_extrapolated": None, "n_basis": N}
+                      f"{qs} quartets in {ts:.1f} s of parallel ERI+digestion time "
+                      f"(partial-matrix merge and the {tq:.1f} s Schwarz diagonal excluded)",
+            "n_basis": N}
 
 
 # ------------------------------------------------------------------ GPU arm

@@ -45,7 +45,12 @@ typedef struct eritile_gpu_stats {
   int gpu_launches_last_build; /* kernels launched by the last build */
 } eritile_gpu_stats;
 
-/* Create a context on CUDA device `device`. Fails if no device. */
+/* Create a context on CUDA device `device`. Fails if no device.
+ * device = -1 creates a host-only context: input parsing, the host Block
+ * Constructor and screened-list construction from a supplied Q
+ * (eritile_gpu_set_schwarz) work; every integral entry point fails with
+ * ERITILE_ERR_CUDA. It exists so the host logic is testable without a GPU;
+ * it is not a CPU fallback. */
 int eritile_gpu_create(int device, eritile_gpu** out);
 void eritile_gpu_destroy(eritile_gpu* ctx);
 const char* eritile_gpu_last_error(const eritile_gpu* ctx);

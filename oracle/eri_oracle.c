@@ -21,6 +21,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 #include <unistd.h>
 
 #define ANG2BOHR 1.8897259886 /* molecule.hpp:16 */
@@ -919,8 +920,9 @@ static void* jk_worker(void* arg) {
   return NULL;
 }
 
-int orc_build_jk_sample(orc_ctx* C, const double* D, double tau, int nthreads, long long stride,
-                        long long offset, double* Jout, double* Kout, long long* nquartets) {
+int orc_build_jk_timed(orc_ctx* C, const double* D, double tau, int nthreads, long long stride,
+                       long long offset, double* Jout, double* Kout, long long* nquartets,
+                       double* seconds) {
   pthread_once(&g_once, init_tables);
   if (tau > 0.0) compute_q(C);
   if (nthreads <= 0) nthreads = default_threads();
@@ -940,7 +942,11 @@ int orc_build_jk_sample(orc_ctx* C, const double* D, double tau, int nthreads, l
     J.Jp[w] = calloc(NN, sizeof(double));
     J.Kp[w] = calloc(NN, sizeof(double));
   }
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
   run_workers(&J, jk_worker);
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  if (seconds) *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
   double* Jm = calloc(NN, sizeof(double));
   double* Km = calloc(NN, sizeof(double));
   long long nq = 0;
@@ -967,9 +973,14 @@ int orc_build_jk_sample(orc_ctx* C, const double* D, double tau, int nthreads, l
   return 0;
 }
 
+int orc_build_jk_sample(orc_ctx* C, const double* D, double tau, int nthreads, long long stride,
+                        long long offset, double* J, double* K, long long* nquartets) {
+  return orc_build_jk_timed(C, D, tau, nthreads, stride, offset, J, K, nquartets, NULL);
+}
+
 int orc_build_jk(orc_ctx* C, const double* D, double tau, int nthreads, double* J, double* K,
                  long long* nquartets) {
-  return orc_build_jk_sample(C, D, tau, nthreads, 1, 0, J, K, nquartets);
+  return orc_build_jk_timed(C, D, tau, nthreads, 1, 0, J, K, nquartets, NULL);
 }
 
 /* ------------------------------------------------- one-electron (SPEC §scf) */

@@ -53,6 +53,10 @@ int orc_build_jk(orc_ctx* c, const double* D, double tau, int nthreads, double* 
 int orc_build_jk_sample(orc_ctx* c, const double* D, double tau, int nthreads,
                         long long stride, long long offset, double* J, double* K,
                         long long* nquartets);
+/* As build_jk_sample; *seconds = wall time of the parallel ERI+digestion
+ * phase only (excludes partial-matrix allocation and merge). */
+int orc_build_jk_timed(orc_ctx* c, const double* D, double tau, int nthreads, long long stride,
+                       long long offset, double* J, double* K, long long* nquartets, double* seconds);
 /* One-electron S, T, V, McMurchie-Davidson; scaled. */
 int orc_one_electron(orc_ctx* c, double* S, double* T, double* V);
 double orc_nuclear_repulsion(orc_ctx* c);

@@ -16,6 +16,7 @@
 // (x,y) iff Q_x*Q_y >= tau.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -227,7 +228,8 @@ void for_each_quartet_in_block(const Ctx& C, const QuadBlock& blk, double tau, F
 }
 
 int build_jk_impl(Ctx& C, const double* D, double tau, int nthreads, long long stride,
-                  long long offset, double* Jout, double* Kout, long long* nq_out) {
+                  long long offset, double* Jout, double* Kout, long long* nq_out,
+                  double* seconds = nullptr) {
   if (tau > 0.0) compute_q(C);
   const std::size_t N = C.nbf, NN = N * N;
   // compile every plan up front (offline step; not part of the build)
@@ -239,6 +241,7 @@ int build_jk_impl(Ctx& C, const double* D, double tau, int nthreads, long long s
   std::atomic<long long> next{0};
   const long long nb = static_cast<long long>(C.blocks.size());
   std::vector<std::thread> th;
+  const auto t0 = std::chrono::steady_clock::now();
   for (int w = 0; w < nthreads; ++w)
     th.emplace_back([&, w] {
       Scratch S;
@@ -252,6 +255,8 @@ int build_jk_impl(Ctx& C, const double* D, double tau, int nthreads, long long s
       }
     });
   for (auto& t : th) t.join();
+  if (seconds)
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   std::vector<double> J(NN, 0.0), K(NN, 0.0);
   for (int w = 0; w < nthreads; ++w)  // merge in worker order
     for (std::size_t e = 0; e < NN; ++e) {
@@ -432,6 +437,16 @@ int ref_build_jk_sample(void* cv, const double* D, double tau, int nthreads, lon
                         long long offset, double* J, double* K, long long* nq) {
   try {
     return build_jk_impl(*static_cast<Ctx*>(cv), D, tau, nthreads, stride, offset, J, K, nq);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_build_jk_timed(void* cv, const double* D, double tau, int nthreads, long long stride,
+                       long long offset, double* J, double* K, long long* nq, double* seconds) {
+  try {
+    return build_jk_impl(*static_cast<Ctx*>(cv), D, tau, nthreads, stride, offset, J, K, nq, seconds);
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

@@ -226,6 +226,7 @@ struct eritile_gpu {
   DevBuf<double> d_D, d_Ds, d_JK, d_J, d_K;
 
   bool profiling = false;
+  bool host_only = false;  // device < 0: block constructor / lists only
   std::vector<cudaEvent_t> prof_ev;
 
   ~eritile_gpu() {
@@ -261,7 +262,7 @@ struct eritile_gpu {
     nbf = bf_off.back();
     have_mol = true;
     have_pairs = have_q = have_lists = false;
-    d_scale.upload(bf_scale);
+    if (!host_only) d_scale.upload(bf_scale);
   }
 
   // block.hpp:52-103 restated + product orientation and grouping.
@@ -365,8 +366,10 @@ struct eritile_gpu {
         groups.push_back(Group{LA, LB, m.K, g, 0});
       groups.back().count++;
     }
-    d_pm.upload(pm);
-    d_prims.upload(prims);
+    if (!host_only) {
+      d_pm.upload(pm);
+      d_prims.upload(prims);
+    }
     have_pairs = true;
     have_q = have_lists = false;
   }
@@ -379,6 +382,7 @@ struct eritile_gpu {
 
   void schwarz() {
     if (!have_pairs) throw StateError("schwarz before build_pairs");
+    if (host_only) throw CudaError("schwarz needs a CUDA device (host-only context)");
     const int np = static_cast<int>(pm.size());
     d_Q.alloc(np);
     std::vector<int> list;
@@ -442,7 +446,7 @@ struct eritile_gpu {
     }
     pm.swap(npm);
     Q.swap(nQ);
-    d_pm.upload(pm);
+    if (!host_only) d_pm.upload(pm);
   }
 
   void set_screening(double t) {
@@ -535,8 +539,10 @@ struct eritile_gpu {
         work.push_back(cw);
       }
     }
-    d_cnt.upload(cnt);
-    d_items.upload(items);
+    if (!host_only) {
+      d_cnt.upload(cnt);
+      d_items.upload(items);
+    }
     have_lists = true;
   }
 
@@ -604,6 +610,7 @@ struct eritile_gpu {
   }
 
   void check_ready() {
+    if (host_only) throw CudaError("build_jk needs a CUDA device (host-only context)");
     if (!have_lists) throw StateError("build_jk before set_screening");
   }
 };
@@ -617,7 +624,7 @@ int fail(eritile_gpu* c, int code, const std::string& m) {
 template <class F>
 int guard(eritile_gpu* c, F&& f) {
   try {
-    if (c) CK(cudaSetDevice(c->device));
+    if (c && !c->host_only) CK(cudaSetDevice(c->device));
     f();
     return ERITILE_OK;
   } catch (const InputError& e) {
@@ -640,6 +647,13 @@ extern "C" {
 int eritile_gpu_create(int device, eritile_gpu** out) {
   if (!out) return ERITILE_ERR_ARG;
   *out = nullptr;
+  if (device < 0) {  // host-only context: input, pairs, screening lists; no kernels
+    auto c = std::make_unique<eritile_gpu>();
+    c->device = -1;
+    c->host_only = true;
+    *out = c.release();
+    return ERITILE_OK;
+  }
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
     g_create_err = "no CUDA device (eritile_gpu has no CPU fallback)";

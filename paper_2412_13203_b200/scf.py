@@ -1,0 +1,109 @@
+"""Closed-shell RHF driver over the GPU Fock build.
+
+The caller of the hot path: one-electron S, T, V (host), X = S^-1/2
+(SPEC.md:464-472), core-Hamiltonian guess, Roothaan iterations with
+F = H + 2J - K from ``Engine.build_jk`` (one GPU Fock build per iteration),
+optional DIIS (depth 6), convergence on the max-abs density
+change (default 1e-6) and max_iter 99 (§7.5).
+E = sum D (H + F) + E_nuc with D = C_occ C_occ^T.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+
+@dataclass
+class ScfResult:
+    energy: float
+    iterations: int
+    converged: bool
+    energies: List[float] = field(default_factory=list)
+    density: Optional[np.ndarray] = None
+    fock_builds: int = 0
+
+
+def orthogonalizer(S: np.ndarray, tol: float = 1e-10) -> np.ndarray:
+    """Symmetric X = S^-1/2; linear dependence is an error."""
+    w, U = np.linalg.eigh(S)
+    if w.min() < tol:
+        raise np.linalg.LinAlgError(f"overlap has eigenvalue {w.min():.3e} < {tol:g} (linear dependence)")
+    return (U * w ** -0.5) @ U.T
+
+
+def density_from_mos(C: np.ndarray, nocc: int) -> np.ndarray:
+    if nocc > C.shape[1]:
+        raise ValueError("n_occ exceeds the basis dimension")
+    Co = C[:, :nocc]
+    return Co @ Co.T
+
+
+def rhf(build_jk: Callable[[np.ndarray], tuple], S: np.ndarray, H: np.ndarray, e_nuc: float, nocc: int,
+        conv: float = 1e-6, max_iter: int = 99, diis: bool = True, damping: float = 0.0,
+        e_conv: float = 1e-10) -> ScfResult:
+    """Roothaan/DIIS loop; ``build_jk(D) -> (J, K)`` is the Fock build."""
+    X = orthogonalizer(S)
+    _, Cp = np.linalg.eigh(X.T @ H @ X)
+    D = density_from_mos(X @ Cp, nocc)
+    res = ScfResult(energy=0.0, iterations=0, converged=False)
+    focks, errs = [], []
+    E_old = None
+    for it in range(1, max_iter + 1):
+        J, K = build_jk(D)
+        res.fock_builds += 1
+        F = H + 2.0 * J - K
+        E = float(np.sum(D * (H + F)) + e_nuc)
+        if not np.isfinite(E):
+            raise FloatingPointError("SCF energy is not finite")
+        res.energies.append(E)
+        Fs = F
+        if diis:
+            err = X.T @ (F @ D @ S - S @ D @ F) @ X
+            focks.append(F)
+            errs.append(err)
+            if len(focks) > 6:
+                focks.pop(0)
+                errs.pop(0)
+            n = len(focks)
+            if n >= 2:
+                B = -np.ones((n + 1, n + 1))
+                B[n, n] = 0.0
+                for a in range(n):
+                    for b in range(n):
+                        B[a, b] = np.sum(errs[a] * errs[b])
+                rhs = np.zeros(n + 1)
+                rhs[n] = -1.0
+                try:
+                    c = np.linalg.solve(B, rhs)[:n]
+                    Fs = sum(ci * Fi for ci, Fi in zip(c, focks))
+                except np.linalg.LinAlgError:
+                    Fs = F
+        _, Cp = np.linalg.eigh(X.T @ Fs @ X)
+        Dn = density_from_mos(X @ Cp, nocc)
+        if damping > 0.0 and not diis:
+            Dn = (1.0 - damping) * Dn + damping * D
+        dD = float(np.max(np.abs(Dn - D)))
+        D = Dn
+        res.iterations = it
+        if dD < conv and (E_old is not None and abs(E - E_old) < e_conv):
+            res.converged = True
+            break
+        E_old = E
+    # final energy with the converged density
+    J, K = build_jk(D)
+    res.fock_builds += 1
+    F = H + 2.0 * J - K
+    res.energy = float(np.sum(D * (H + F)) + e_nuc)
+    res.density = D
+    return res
+
+
+def run_rhf(xyz_text: str, basis_text: str, tau: float = 1e-12, device: int = 0, **kw) -> ScfResult:
+    """Full driver on one GPU: load, pairs, Schwarz, screening, SCF."""
+    from .eritile import Engine
+    e = Engine(device).load_molecule(xyz_text, basis_text).build_pairs(0.0)
+    e.set_screening(tau)
+    S, T, V = e.one_electron()
+    return rhf(e.build_jk, S, T + V, e.nuclear_repulsion(), e.nelectrons // 2, **kw)

@@ -73,6 +73,8 @@ class Oracle:
         f("build_jk", C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, _dp, _dp, C.POINTER(C.c_longlong)])
         f("build_jk_sample", C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_longlong,
                                         C.c_longlong, _dp, _dp, C.POINTER(C.c_longlong)])
+        f("build_jk_timed", C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_longlong, C.c_longlong,
+                                       _dp, _dp, C.POINTER(C.c_longlong), C.POINTER(C.c_double)])
         if kind == "orc":
             f("one_electron", C.c_int, [C.c_void_p, _dp, _dp, _dp])
             f("nuclear_repulsion", C.c_double, [C.c_void_p])
@@ -179,6 +181,19 @@ class System:
         if rc != 0:
             raise RuntimeError(self.o._last_error().decode())
         return J, K, nq.value
+
+    def build_jk_timed(self, D: np.ndarray, tau: float, nthreads: int, stride: int, offset: int):
+        """(J, K, quartets, seconds of the parallel ERI+digestion phase)."""
+        N = self.nbf
+        D = np.ascontiguousarray(D, dtype=np.float64)
+        J = np.zeros((N, N))
+        K = np.zeros((N, N))
+        nq = C.c_longlong(0)
+        sec = C.c_double(0.0)
+        rc = self.o._build_jk_timed(self.h, D, tau, nthreads, stride, offset, J, K, C.byref(nq), C.byref(sec))
+        if rc != 0:
+            raise RuntimeError(self.o._last_error().decode())
+        return J, K, nq.value, sec.value
 
     def one_electron(self):
         N = self.nbf
