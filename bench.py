@@ -41,6 +41,11 @@ def parse():
     ap.add_argument("--waters", type=int, default=80)
     ap.add_argument("--basis", default="cc-pvdz")
     ap.add_argument("--tau", type=float, default=1e-10)
+    ap.add_argument("--kappa", type=float, default=1e-14,
+                    help="reference primitive-pair screen |coef|*kappa < thr (block.hpp:83-89; "
+                         "SPEC.md:188 flag value 1e-14; 0 = off). Both arms use the same value.")
+    ap.add_argument("--no-unscreened", action="store_true",
+                    help="skip the secondary kappa-off measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample length")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -62,8 +67,9 @@ def synthetic_density(N: int, nocc: int, seed: int = 2412) -> np.ndarray:
 
 
 def config(args, nranks):
-    return {"workload": f"(H2O)_{args.waters}/{args.basis} RHF Fock build (ERI + J/K), Schwarz tau={args.tau:g}",
-            "n_basis": None, "tau": args.tau, "basis": args.basis, "waters": args.waters,
+    return {"workload": f"(H2O)_{args.waters}/{args.basis} RHF Fock build (ERI + J/K), Schwarz tau={args.tau:g}, "
+                        f"kappa screen {args.kappa:g}",
+            "n_basis": None, "tau": args.tau, "kappa_screen": args.kappa, "basis": args.basis, "waters": args.waters,
             "density": "synthetic C_occ C_occ^T (seeded QR)", "parallelism": f"quartet-shard x{nranks} + NCCL allreduce(J,K)",
             "l2": "256 MiB buffer written between timed steps (L2 flush)"}
 
@@ -152,7 +158,7 @@ def cpu_sample(args, steps: int, warmup: int, target_s: float, reference_arm: bo
     kind = "reference" if available("ref") else "port"
     o = Oracle("ref" if kind == "reference" else "orc")
     xyz, basis = workload(args)
-    S = o.system(xyz, basis)
+    S = o.system(xyz, basis, kappa_screen=args.kappa)
     N = S.nbf
     D = synthetic_density(N, S.nelectrons // 2)
     cores = os.cpu_count() or 1
@@ -198,7 +204,7 @@ def run_ours(args, rank, nranks, local_rank):
 
     xyz, basis = workload(args)
     t0 = time.perf_counter()
-    eng = Engine(local_rank).load_molecule(xyz, basis).build_pairs(0.0)
+    eng = Engine(local_rank).load_molecule(xyz, basis).build_pairs(args.kappa)
     eng.set_shard(rank, nranks)
     eng.set_screening(args.tau)
     setup_s = time.perf_counter() - t0
@@ -214,6 +220,14 @@ def run_ours(args, rank, nranks, local_rank):
     J = torch.empty((N, N), dtype=torch.float64, device=dev)
     K = torch.empty((N, N), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # Workload Allocator: per-class kernel variant chosen on the live density
+    # before the warm-up builds (untimed, like the reference's tune during
+    # the first SCF iterations)
+    t1 = time.perf_counter()
+    eng.tune(Dh, reps=3)
+    tune_s = time.perf_counter() - t1
+    chosen = eng.variants()
 
     def step():
         eng.build_jk_partial_device(D.data_ptr(), JK.data_ptr(), sp)
@@ -266,6 +280,29 @@ def run_ours(args, rank, nranks, local_rank):
     prof = eng.class_profile()
     eng.set_profiling(False)
 
+    # secondary: the same build with the primitive-pair screen off (the
+    # reference's default), for transparency (not the headline)
+    kappa_off = None
+    if args.kappa > 0 and not args.no_unscreened and nranks == 1:
+        del eng
+        e0 = Engine(local_rank).load_molecule(xyz, basis).build_pairs(0.0)
+        e0.set_screening(args.tau)
+        s0 = e0.stats()
+        e0.build_jk_partial_device(D.data_ptr(), JK.data_ptr(), sp)
+        ev0 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+        for k in range(2):
+            flush.fill_(float(k))
+            ev0[k][0].record(stream)
+            e0.build_jk_partial_device(D.data_ptr(), JK.data_ptr(), sp)
+            e0.finalize_device(JK.data_ptr(), J.data_ptr(), K.data_ptr(), sp)
+            ev0[k][1].record(stream)
+        torch.cuda.synchronize()
+        ms0 = sum(a.elapsed_time(b) for a, b in ev0) / 2
+        kappa_off = {"kappa_screen": 0.0, "ms_per_step": ms0, "quartets_per_build": s0["quartets"],
+                     "prim_quartets_per_build": s0["prim_quartets"], "value": s0["quartets"] / (ms0 * 1e-3),
+                     "unit": UNIT, "steps": 2, "warmup": 1}
+        del e0
+
     q_local = st["quartets"]
     pq_local = st["prim_quartets"]
     fl_local = st["model_flops"]
@@ -305,10 +342,13 @@ def run_ours(args, rank, nranks, local_rank):
         "e2e": {"value": q_tot / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * N * N,
                 "d2h_bytes_per_step": 16 * N * N, "ms_per_step": e2e_ms},
         "gpu_launches": launches * args.steps,
+        "kappa_off": kappa_off,
         "roofline": roof,
         "clocks": clk.summary(),
         "setup_s": setup_s,
+        "tune_s": tune_s,
         "classes": [{"cls": "".join(map(str, r["cls"])), "ms": round(r["ms"], 4),
+                     "variant": chosen.get(tuple(r["cls"])),
                      "tflops": r["flops"] / max(r["ms"], 1e-9) / 1e9, "quartets": r["quartets"]}
                     for r in sorted(prof, key=lambda r: -r["ms"])],
     }

@@ -129,6 +129,17 @@ int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out);
 int eritile_gpu_set_profiling(eritile_gpu* ctx, int on);
 int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, double* flops,
                               long long* quartets, long long* prim_quartets);
+/* Workload Allocator (Alg. 2; SPEC.md:367-438 tune): time
+ * every kernel variant of every class launch of this rank on density D
+ * (host, N x N), median of `reps` launches each, and keep the fastest per
+ * class. Variants: "lane_m2"/"lane_m3" (one lane per quartet, straight-line
+ * plan, residency target 2/3 CTAs per SM) and "coop" (CTA-cooperative
+ * level-scheduled plan). The choice changes atomic summation order only. */
+int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps);
+int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var);
+int eritile_gpu_get_variant(const eritile_gpu* ctx, int cls_index);
+int eritile_gpu_class_nvariants(int cls_index);
+const char* eritile_gpu_variant_name(int cls_index, int var);
 /* Plan statistics of the generated class kernels, i < num_classes:
  * la lb lc ld max_m ops prim_terms base contract hrr_terms. */
 int eritile_gpu_num_classes(void);

@@ -895,9 +895,11 @@ static void* jk_worker(void* arg) {
   double* out = malloc(sizeof(double) * 50625); /* (g g|g g) */
   long long nq = 0;
   for (;;) {
-    long long bi = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+    /* only the sampled blocks offset, offset + stride, ... are claimed */
+    const long long st = J->stride > 1 ? J->stride : 1, o0 = J->stride > 1 ? J->offset : 0;
+    const long long k = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+    const long long bi = o0 + k * st;
     if (bi >= C->nblock) break;
-    if (J->stride > 1 && bi % J->stride != J->offset) continue;
     const tile_t* ti = &C->tl[C->bl[bi].bt];
     const tile_t* tj = &C->tl[C->bl[bi].kt];
     for (int x = ti->first; x < ti->first + ti->count; ++x) {

@@ -245,8 +245,9 @@ int build_jk_impl(Ctx& C, const double* D, double tau, int nthreads, long long s
   for (int w = 0; w < nthreads; ++w)
     th.emplace_back([&, w] {
       Scratch S;
-      for (long long bi; (bi = next.fetch_add(1)) < nb;) {
-        if (stride > 1 && bi % stride != offset) continue;
+      // only the sampled blocks offset, offset + stride, ... are claimed
+      const long long st = stride > 1 ? stride : 1, o0 = stride > 1 ? offset : 0;
+      for (long long bi; (bi = o0 + next.fetch_add(1) * st) < nb;) {
         for_each_quartet_in_block(C, C.blocks[bi], tau, [&](int x, int y) {
           quartet_scaled(C, x, y, S);
           digest(C, x, y, S.v.data(), D, Jp[w].data(), Kp[w].data());

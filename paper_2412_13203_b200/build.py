@@ -32,8 +32,7 @@ INCLUDE = ROOT / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
-                  "-I" + str(INCLUDE), "-I" + str(CSRC),
-                  "-DERITILE_JK_MINB=" + os.environ.get("ERITILE_JK_MINB", "2")]
+                  "-I" + str(INCLUDE), "-I" + str(CSRC)]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread", "-I" + str(INCLUDE),
             "-I" + str(CSRC), "-I/usr/local/cuda/include"]
 LMAX = int(os.environ.get("ERITILE_LMAX", "2"))
@@ -70,7 +69,7 @@ def build(jobs: int | None = None, verbose: bool = True) -> Path:
     OBJ.mkdir(exist_ok=True)
     LIBDIR.mkdir(exist_ok=True)
     generate()
-    kern_deps = [CSRC / "jk_kernels.cuh", CSRC / "jk_api.h"]
+    kern_deps = [CSRC / "jk_kernels.cuh", CSRC / "jk_coop.cuh", CSRC / "jk_api.h"]
     host_deps = [CSRC / "host" / "molecule.h", CSRC / "host" / "onee.h", CSRC / "jk_api.h",
                  INCLUDE / "eritile_gpu.h"]
     units = []

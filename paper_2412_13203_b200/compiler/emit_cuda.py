@@ -233,7 +233,39 @@ def emit_class(cls) -> Tuple[str, Dict]:
     return "\n".join(lines) + "\n", info
 
 
+# Variant policy (the Workload Allocator picks among these at run time,
+# csrc/host/engine.cu tune()): one-lane-per-quartet straight-line kernels
+# for plans up to LANE_MAX_OPS operations, in MINB_VARIANTS occupancy
+# flavours for the small plans; CTA-cooperative table kernels (compiler/
+# coop.py) for plans of at least COOP_MIN_OPS operations.
+LANE_MAX_OPS = int(os.environ.get("ERITILE_LANE_MAX_OPS", "4000"))
+COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
+MINB_SMALL_OPS = 700
+MINB_VARIANTS = (2, 3)
+
+
+def variants(info) -> List[Tuple[str, str]]:
+    """(name, launcher expression) per kernel variant of one class."""
+    cid = class_id(info["cls"])
+    out = []
+    if info["ops"] <= LANE_MAX_OPS:
+        mins = MINB_VARIANTS if info["ops"] <= MINB_SMALL_OPS else (2,)
+        for m in mins:
+            out.append((f"lane_m{m}", f"launch_class<Cls{cid}, {m}>"))
+    if info["ops"] >= COOP_MIN_OPS:
+        out.append(("coop", f"launch_coop_cls{cid}"))
+    return out
+
+
+def default_variant(info, vs) -> int:
+    names = [v[0] for v in vs]
+    if "coop" in names and (info["ops"] >= 2000 or len(names) == 1):
+        return names.index("coop")
+    return 0
+
+
 def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
+    from .coop import emit_tables, schedule
     outdir.mkdir(parents=True, exist_ok=True)
     infos = []
     classes = canonical_classes(lmax)
@@ -241,33 +273,69 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         body, info = emit_class(cls)
         cid = class_id(cls)
         info["index"] = idx
+        vs = variants(info)
+        info["variants"] = vs
+        info["default"] = default_variant(info, vs)
         infos.append(info)
-        src = [
-            "// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
-            '#include "../jk_kernels.cuh"',
-            "namespace eritile_b200 {",
-            body,
-            f"void launch_cls{cid}(const LaunchArgs& a) {{ launch_class<Cls{cid}>(a); }}",
-            "}  // namespace eritile_b200",
-            "",
-        ]
+        lane = any(n.startswith("lane") for n, _ in vs)
+        coop = any(n == "coop" for n, _ in vs)
+        src = ["// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
+               '#include "../jk_coop.cuh"', "namespace eritile_b200 {"]
+        if lane:
+            src.append(body)
+        else:  # sizes only; the straight-line body is not emitted
+            na, nb, nc, nd = map(ncart, cls)
+            src.append(f"struct Cls{cid} {{\n  static constexpr int LA = {cls[0]}, LB = {cls[1]}, "
+                       f"LC = {cls[2]}, LD = {cls[3]};\n  static constexpr int NA = {na}, NB = {nb}, "
+                       f"NC = {nc}, ND = {nd};\n  static constexpr int NV = {na * nb * nc * nd};\n"
+                       f"  static constexpr int M = {info['M']};\n  static constexpr int OPS = {info['ops']};\n}};")
+        if coop:
+            sc = schedule(cls)
+            width = max(b - a for a, b in zip(sc["lo_lvl"], sc["lo_lvl"][1:]))
+            nt = 256 if width >= 192 else 128
+            src.append(emit_tables(cid, sc))
+            src.append(f"struct CoopCls{cid} : Cls{cid} {{ static constexpr int NT = {nt}; }};")
+            src.append(f"void launch_coop_cls{cid}(const LaunchArgs& a) {{")
+            src.append("  CoopTables t{};")
+            for fld, sym in [("lo", "kLo"), ("lo_lvl", "kLoLvl"), ("bd", "kBd"), ("up", "kUp"),
+                             ("up_lvl", "kUpLvl"), ("combo", "kCombo"), ("tgt", "kTgt")]:
+                src.append(f"  cudaGetSymbolAddress((void**)&t.{fld}, {sym}{cid});")
+            src.append(f"  t.nlo_lvl = {len(sc['lo_lvl']) - 1}; t.nb = {sc['nb']}; "
+                       f"t.nup_lvl = {len(sc['up_lvl']) - 1}; t.ncombo = {len(sc['combo'])}; "
+                       f"t.nslots = {sc['nslots']};")
+            src.append(f"  launch_coop<CoopCls{cid}>(t, a);")
+            src.append("}")
+        for name, expr in vs:
+            if name.startswith("lane"):
+                src.append(f"void launch_{name}_cls{cid}(const LaunchArgs& a) {{ {expr}(a); }}")
+        src += ["}  // namespace eritile_b200", ""]
         _write_if_changed(outdir / f"cls_{cid}.cu", "\n".join(src))
     reg = ["// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
            '#include "../jk_api.h"', "namespace eritile_b200 {"]
+    def fn(name, cid):
+        return f"launch_coop_cls{cid}" if name == "coop" else f"launch_{name}_cls{cid}"
     for info in infos:
-        reg.append(f"void launch_cls{class_id(info['cls'])}(const LaunchArgs&);")
+        cid = class_id(info["cls"])
+        for name, _ in info["variants"]:
+            reg.append(f"void {fn(name, cid)}(const LaunchArgs&);")
     reg.append("const ClassEntry kClassTable[] = {")
     for info in infos:
         la, lb, lc, ld = info["cls"]
         cid = class_id(info["cls"])
+        vs = info["variants"]
+        fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (4 - len(vs))
+        names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (4 - len(vs))
         reg.append(f"  {{{la}, {lb}, {lc}, {ld}, {info['M']}, {info['ops']}, {info['prim_terms']}, "
-                   f"{info['base']}, {info['contract']}, {info['hrr_terms']}, "
-                   f"&launch_cls{cid}}},")
+                   f"{info['base']}, {info['contract']}, {info['hrr_terms']}, {len(vs)}, {{{fns}}}, "
+                   f"{{{names}}}, {info['default']}}},")
     reg.append("};")
     reg.append(f"const int kNumClasses = {len(infos)};")
     reg.append(f"const int kMaxL = {lmax};")
     reg.append("}  // namespace eritile_b200")
     _write_if_changed(outdir / "registry.cpp", "\n".join(reg) + "\n")
+    for stale in outdir.glob("cls_*.cu"):
+        if stale.stem[4:] not in {class_id(i["cls"]) for i in infos}:
+            stale.unlink()
     return infos
 
 

@@ -225,6 +225,10 @@ struct eritile_gpu {
   DevBuf<int> d_list;
   DevBuf<double> d_D, d_Ds, d_JK, d_J, d_K;
 
+  // Workload Allocator state: kernel variant per class (kClassTable[c].var)
+  std::vector<int> var_choice;
+  std::vector<double> tune_ms;  // per class launch: best measured ms (tune)
+
   bool profiling = false;
   bool host_only = false;  // device < 0: block constructor / lists only
   std::vector<cudaEvent_t> prof_ev;
@@ -234,6 +238,77 @@ struct eritile_gpu {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
+  }
+
+  int variant(int c) const {
+    return var_choice.empty() ? kClassTable[c].def : var_choice[c];
+  }
+
+  // Workload Allocator (Alg. 2): for every
+  // class launch of this rank, time each kernel variant (median of R
+  // launches, CUDA events) on the live density and keep the fastest. The
+  // reference tunes a granularity g by doubling; here the tuned knob is the
+  // variant (lane kernel residency / CTA-cooperative split), whose choice
+  // cannot change results beyond atomic summation order.
+  void tune(const double* dDs, int reps) {
+    if (var_choice.empty()) {
+      var_choice.resize(kNumClasses);
+      for (int c = 0; c < kNumClasses; ++c) var_choice[c] = kClassTable[c].def;
+    }
+    const size_t NN = static_cast<size_t>(nbf) * nbf;
+    DevBuf<double> scratch;
+    scratch.alloc(2 * NN);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    tune_ms.assign(work.size(), 0.0);
+    for (size_t w = 0; w < work.size(); ++w) {
+      const ClassWork& cw = work[w];
+      const ClassEntry& ce = kClassTable[cw.cls];
+      double best = 1e300;
+      int bestv = var_choice[cw.cls];
+      for (int v = 0; v < ce.nvar; ++v) {
+        std::vector<double> t;
+        for (int r = 0; r < reps + 1; ++r) {
+          LaunchArgs a = class_args(cw, dDs, scratch.p, stream);
+          CK(cudaEventRecord(e0, stream));
+          ce.var[v](a);
+          CK(cudaGetLastError());
+          CK(cudaEventRecord(e1, stream));
+          CK(cudaEventSynchronize(e1));
+          if (r > 0) t.push_back(elapsed(e0, e1));  // first launch warms up
+        }
+        std::sort(t.begin(), t.end());
+        const double med = t[t.size() / 2];
+        if (med < best) {
+          best = med;
+          bestv = v;
+        }
+      }
+      var_choice[cw.cls] = bestv;
+      tune_ms[w] = best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+
+  LaunchArgs class_args(const ClassWork& cw, const double* dDs, double* dJK, cudaStream_t st) const {
+    const size_t NN = static_cast<size_t>(nbf) * nbf;
+    LaunchArgs a{};
+    a.mode = 0;
+    a.items = d_items.p + cw.off;
+    a.nitems = cw.n;
+    a.cnt = d_cnt.p;
+    a.pm = d_pm.p;
+    a.prims = d_prims.p;
+    a.D = dDs;
+    a.J = dJK;
+    a.K = dJK + NN;
+    a.N = nbf;
+    a.boys_tab = d_boys.p;
+    a.stream = st;
+    a.block = 128;
+    return a;
   }
 
   int class_index(int la, int lb, int lc, int ld) const {
@@ -407,7 +482,7 @@ struct eritile_gpu {
       a.boys_tab = d_boys.p;
       a.stream = stream;
       a.block = 128;
-      ce.launch(a);
+      ce.var[variant(c)](a);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(stream));
     }
@@ -567,21 +642,8 @@ struct eritile_gpu {
     for (size_t w = 0; w < work.size(); ++w) {
       const ClassWork& cw = work[w];
       if (profiling) CK(cudaEventRecord(prof_ev[2 * w], st));
-      LaunchArgs a{};
-      a.mode = 0;
-      a.items = d_items.p + cw.off;
-      a.nitems = cw.n;
-      a.cnt = d_cnt.p;
-      a.pm = d_pm.p;
-      a.prims = d_prims.p;
-      a.D = dDs;
-      a.J = dJK;
-      a.K = dJK + NN;
-      a.N = nbf;
-      a.boys_tab = d_boys.p;
-      a.stream = st;
-      a.block = 128;
-      kClassTable[cw.cls].launch(a);
+      LaunchArgs a = class_args(cw, dDs, dJK, st);
+      kClassTable[cw.cls].var[variant(cw.cls)](a);
       CK(cudaGetLastError());
       ++launches_last;
       if (profiling) CK(cudaEventRecord(prof_ev[2 * w + 1], st));
@@ -940,7 +1002,7 @@ int eritile_gpu_eri_quartet(eritile_gpu* ctx, int x, int y, double* out) {
     a.boys_tab = ctx->d_boys.p;
     a.stream = ctx->stream;
     a.block = 128;
-    kClassTable[cls].launch(a);
+    kClassTable[cls].var[ctx->variant(cls)](a);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     std::vector<double> v(nv);
@@ -1016,6 +1078,44 @@ int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out) {
   out->last_schwarz_ms = ctx->last_schwarz_ms;
   out->gpu_launches_last_build = ctx->launches_last;
   return ERITILE_OK;
+}
+
+int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps) {
+  if (!ctx || !D || reps < 1) return ERITILE_ERR_ARG;
+  return guard(ctx, [&] {
+    ctx->check_ready();
+    ctx->ensure_mats();
+    const size_t NN = static_cast<size_t>(ctx->nbf) * ctx->nbf;
+    ctx->d_D.alloc(NN);
+    CK(cudaMemcpy(ctx->d_D.p, D, sizeof(double) * NN, cudaMemcpyHostToDevice));
+    ctx->prescale(ctx->d_D.p, ctx->d_Ds.p, ctx->stream);
+    ctx->tune(ctx->d_Ds.p, reps);
+  });
+}
+
+int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var) {
+  if (!ctx || cls_index < 0 || cls_index >= kNumClasses) return ERITILE_ERR_ARG;
+  if (var < 0 || var >= kClassTable[cls_index].nvar) return fail(ctx, ERITILE_ERR_ARG, "no such kernel variant");
+  if (ctx->var_choice.empty()) {
+    ctx->var_choice.resize(kNumClasses);
+    for (int c = 0; c < kNumClasses; ++c) ctx->var_choice[c] = kClassTable[c].def;
+  }
+  ctx->var_choice[cls_index] = var;
+  return ERITILE_OK;
+}
+
+int eritile_gpu_get_variant(const eritile_gpu* ctx, int cls_index) {
+  if (!ctx || cls_index < 0 || cls_index >= kNumClasses) return ERITILE_ERR_ARG;
+  return ctx->variant(cls_index);
+}
+
+int eritile_gpu_class_nvariants(int i) {
+  return (i < 0 || i >= kNumClasses) ? ERITILE_ERR_ARG : kClassTable[i].nvar;
+}
+
+const char* eritile_gpu_variant_name(int i, int v) {
+  if (i < 0 || i >= kNumClasses || v < 0 || v >= kClassTable[i].nvar) return nullptr;
+  return kClassTable[i].var_name[v];
 }
 
 int eritile_gpu_num_classes(void) { return kNumClasses; }

@@ -1,0 +1,267 @@
+// CTA-cooperative ERI + J/K kernel for high-L classes (Deconstruction).
+//
+// One CTA evaluates one contracted quartet at a time from the level-scheduled
+// plan tables of compiler/coop.py: per primitive quartet warp 0 binds the
+// geometry and Boys values (boys.hpp:23-44 semantics,
+// boys_eval) into a small coefficient table, then all threads sweep the
+// primitive-segment levels (vertical recurrences), fold the boundary into the
+// contracted accumulators (compiler.hpp:143), and after the primitive loop
+// sweep the horizontal levels (compiler.hpp:144). All values live in shared
+// memory; one barrier per level. Digestion then spreads the six J/K blocks
+// of SPEC.md:350 over the threads, one FP64 atomic per output element.
+#pragma once
+#include "jk_kernels.cuh"
+
+namespace eritile_b200 {
+
+// base coefficient ids (compiler/coop.py)
+constexpr int kB_PA = 1, kB_QC = 4, kB_WP = 7, kB_WQ = 10, kB_I2P = 13, kB_I2Q = 14, kB_I2PQ = 15,
+              kB_ITP = 16, kB_ITQ = 17, kB_AB = 18, kB_CD = 21, kB_PF = 24;
+constexpr int kCoopMaxCombo = 64;
+constexpr int kCoopBase = 48;  // >= kB_PF + M + 1 for M <= 16
+
+struct CoopTables {
+  const unsigned* lo;
+  const int* lo_lvl;
+  int nlo_lvl;
+  const unsigned* bd;
+  int nb;
+  const unsigned* up;
+  const int* up_lvl;
+  int nup_lvl;
+  const unsigned* combo;
+  int ncombo;
+  const unsigned short* tgt;
+  int nslots;
+};
+
+template <class C>
+struct CoopSmem {
+  static constexpr size_t boys = sizeof(double) * kBoysRows * kBoysCols;
+  static size_t bytes(int nslots) {
+    return boys + sizeof(double) * (kCoopBase + kCoopMaxCombo + nslots) +
+           ((sizeof(unsigned short) * C::NV + 15) & ~size_t(15));
+  }
+};
+
+// Evaluate one contracted quartet; outputs end in val[tgt[k]], kernel order.
+template <class C>
+__device__ __forceinline__ void coop_eval(const CoopTables& tb, const PairMeta& bm, const PairMeta& km,
+                                          const PrimRec* __restrict__ prims, const double* s_boys,
+                                          double* coefb, double* cf, double* val) {
+  const int tid = threadIdx.x;
+  for (int s = tid; s < tb.nb; s += C::NT) val[1 + s] = 0.0;
+  const PrimRec* bra = prims + bm.prim_off;
+  const PrimRec* ket = prims + km.prim_off;
+  const int np = bm.K * km.K;
+  for (int pq = 0; pq < np; ++pq) {
+    if (tid < 32) {
+      const PrimRec bp = load_prim<true>(bra + pq / km.K);
+      const PrimRec kp = load_prim<true>(ket + pq % km.K);
+      const double s = bp.p + kp.p;
+      const double rs = rsqrt_pos(s);
+      const double inv = rs * rs;
+      const double PQx = bp.Px - kp.Px, PQy = bp.Py - kp.Py, PQz = bp.Pz - kp.Pz;
+      const double pinv = bp.p * inv, qinv = kp.p * inv;
+      const double rho = bp.p * qinv;
+      const double T = rho * fma(PQx, PQx, fma(PQy, PQy, PQz * PQz));
+      const double pref = bp.U * kp.U * rs;
+      double F[C::M + 1];
+      boys_eval<C::M>(T, s_boys, F);
+      const int lane = tid;
+      if (lane == 0) {
+        coefb[0] = 1.0;
+        coefb[kB_PA] = bp.PAx; coefb[kB_PA + 1] = bp.PAy; coefb[kB_PA + 2] = bp.PAz;
+        coefb[kB_QC] = kp.PAx; coefb[kB_QC + 1] = kp.PAy; coefb[kB_QC + 2] = kp.PAz;
+        coefb[kB_WP] = -qinv * PQx; coefb[kB_WP + 1] = -qinv * PQy; coefb[kB_WP + 2] = -qinv * PQz;
+        coefb[kB_WQ] = pinv * PQx; coefb[kB_WQ + 1] = pinv * PQy; coefb[kB_WQ + 2] = pinv * PQz;
+      } else if (lane == 1) {
+        coefb[kB_I2P] = bp.i2p;
+        coefb[kB_I2Q] = kp.i2p;
+        coefb[kB_I2PQ] = 0.5 * inv;
+        coefb[kB_ITP] = bp.i2p * qinv;
+        coefb[kB_ITQ] = kp.i2p * pinv;
+        coefb[kB_AB] = bm.ABx; coefb[kB_AB + 1] = bm.ABy; coefb[kB_AB + 2] = bm.ABz;
+        coefb[kB_CD] = km.ABx; coefb[kB_CD + 1] = km.ABy; coefb[kB_CD + 2] = km.ABz;
+      } else if (lane == 2) {
+#pragma unroll
+        for (int m = 0; m <= C::M; ++m) coefb[kB_PF + m] = pref * F[m];
+      }
+      __syncwarp();
+      for (int k = lane; k < tb.ncombo; k += 32) {
+        const unsigned w = __ldg(tb.combo + k);
+        cf[k] = static_cast<double>(static_cast<int>(w >> 8) - 128) * coefb[w & 0xff];
+      }
+    }
+    __syncthreads();
+    // primitive segment, level by level
+    for (int L = 0; L < tb.nlo_lvl; ++L) {
+      const int e = __ldg(tb.lo_lvl + L + 1);
+      for (int o = __ldg(tb.lo_lvl + L) + tid; o < e; o += C::NT) {
+        const uint4* op = reinterpret_cast<const uint4*>(tb.lo) + 2 * o;
+        const uint4 h = __ldg(op);
+        const int nt = h.x >> 16;
+        double acc = cf[h.y >> 16] * val[h.y & 0xffff];
+        if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
+        if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
+        if (nt > 3) {
+          const uint4 g = __ldg(op + 1);
+          acc = fma(cf[g.x >> 16], val[g.x & 0xffff], acc);
+          if (nt > 4) acc = fma(cf[g.y >> 16], val[g.y & 0xffff], acc);
+        }
+        val[h.x & 0xffff] = acc;
+      }
+      __syncthreads();
+    }
+    for (int k = tid; k < tb.nb; k += C::NT) {
+      const unsigned w = __ldg(tb.bd + k);
+      val[w >> 16] += val[w & 0xffff];
+    }
+    __syncthreads();
+  }
+  // contracted horizontal segment
+  for (int L = 0; L < tb.nup_lvl; ++L) {
+    const int e = __ldg(tb.up_lvl + L + 1);
+    for (int o = __ldg(tb.up_lvl + L) + tid; o < e; o += C::NT) {
+      const uint4 h = __ldg(reinterpret_cast<const uint4*>(tb.up) + o);
+      const int nt = h.x >> 16;
+      double acc = cf[h.y >> 16] * val[h.y & 0xffff];
+      if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
+      if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
+      val[h.x & 0xffff] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT) coop_kernel(CoopTables tb, LaunchArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  double* s_boys = smem;
+  double* coefb = s_boys + kBoysRows * kBoysCols;
+  double* cf = coefb + kCoopBase;
+  double* val = cf + kCoopMaxCombo;
+  unsigned short* tgt = reinterpret_cast<unsigned short*>(val + tb.nslots);
+  load_boys_slice(s_boys, a.boys_tab, C::M);
+  for (int k = threadIdx.x; k < C::NV; k += C::NT) tgt[k] = __ldg(tb.tgt + k);
+  if (threadIdx.x == 0) val[0] = 1.0;
+  __syncthreads();
+  const int tid = threadIdx.x;
+
+  if (a.mode == 1 || a.mode == 2) {  // Schwarz diagonal / raw quartets
+    const long long n = a.mode == 1 ? a.npair_list : a.nq;
+    for (long long i = blockIdx.x; i < n; i += gridDim.x) {
+      const int xb = a.mode == 1 ? a.pair_list[i] : a.qpairs[2 * i];
+      const int xk = a.mode == 1 ? xb : a.qpairs[2 * i + 1];
+      const PairMeta bm = a.pm[xb], km = a.pm[xk];
+      coop_eval<C>(tb, bm, km, a.prims, s_boys, coefb, cf, val);
+      if (a.mode == 2) {
+        for (int k = tid; k < C::NV; k += C::NT) a.qout[i * C::NV + k] = val[tgt[k]];
+      } else if (tid < 32) {
+        double mx = 0.0;
+        for (int ab = tid; ab < C::NA * C::NB; ab += 32) {
+          const int ia = ab / C::NB, ib = ab % C::NB;
+          const double s = comp_scale(C::LA, ia) * comp_scale(C::LB, ib);
+          mx = fmax(mx, fabs(val[tgt[(ab * C::NC + ia) * C::ND + ib]]) * (s * s));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (tid == 0) a.Qout[xb] = sqrt(mx);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+
+  const size_t n = static_cast<size_t>(a.N);
+  constexpr int NA = C::NA, NB = C::NB, NC = C::NC, ND = C::ND;
+  constexpr int O1 = NA * NB, O2 = O1 + NC * ND, O3 = O2 + NA * NC, O4 = O3 + NB * ND, O5 = O4 + NA * ND,
+                O6 = O5 + NB * NC;
+  for (long long w = blockIdx.x; w < a.nitems; w += gridDim.x) {
+    const WorkItem it = a.items[w];
+    const int nq = it.r0nq >> 24;
+    int q = it.r0nq & 0xffffff, x = it.bra0, c = it.cntp;
+    for (int l = 0; l < nq; ++l, ++q) {
+      for (int cn = __ldg(a.cnt + c); q >= cn; cn = __ldg(a.cnt + c)) {
+        q -= cn;
+        ++x;
+        ++c;
+      }
+      const int y = it.yfirst + q;
+      const PairMeta bm = a.pm[x], km = a.pm[y];
+      coop_eval<C>(tb, bm, km, a.prims, s_boys, coefb, cf, val);
+      const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (x != y ? 2.0 : 1.0);
+      const double wj = 0.5 * deg, wk = 0.25 * deg;
+      for (int o = tid; o < O6; o += C::NT) {
+        double s = 0.0;
+        double* dst;
+        if (o < O1) {  // J_ab += sum_cd v D_cd
+          const int ia = o / NB, ib = o % NB;
+          for (int ic = 0; ic < NC; ++ic)
+            for (int id = 0; id < ND; ++id)
+              s = fma(val[tgt[((ia * NB + ib) * NC + ic) * ND + id]], __ldg(a.D + (km.bfa + ic) * n + km.bfb + id), s);
+          dst = a.J + (bm.bfa + ia) * n + bm.bfb + ib;
+          s *= wj;
+        } else if (o < O2) {  // J_cd += sum_ab v D_ab
+          const int ic = (o - O1) / ND, id = (o - O1) % ND;
+          for (int ia = 0; ia < NA; ++ia)
+            for (int ib = 0; ib < NB; ++ib)
+              s = fma(val[tgt[((ia * NB + ib) * NC + ic) * ND + id]], __ldg(a.D + (bm.bfa + ia) * n + bm.bfb + ib), s);
+          dst = a.J + (km.bfa + ic) * n + km.bfb + id;
+          s *= wj;
+        } else if (o < O3) {  // K_ac += sum_bd v D_bd
+          const int ia = (o - O2) / NC, ic = (o - O2) % NC;
+          for (int ib = 0; ib < NB; ++ib)
+            for (int id = 0; id < ND; ++id)
+              s = fma(val[tgt[((ia * NB + ib) * NC + ic) * ND + id]], __ldg(a.D + (bm.bfb + ib) * n + km.bfb + id), s);
+          dst = a.K + (bm.bfa + ia) * n + km.bfa + ic;
+          s *= wk;
+        } else if (o < O4) {  // K_bd += sum_ac v D_ac
+          const int ib = (o - O3) / ND, id = (o - O3) % ND;
+          for (int ia = 0; ia < NA; ++ia)
+            for (int ic = 0; ic < NC; ++ic)
+              s = fma(val[tgt[((ia * NB + ib) * NC + ic) * ND + id]], __ldg(a.D + (bm.bfa + ia) * n + km.bfa + ic), s);
+          dst = a.K + (bm.bfb + ib) * n + km.bfb + id;
+          s *= wk;
+        } else if (o < O5) {  // K_ad += sum_bc v D_bc
+          const int ia = (o - O4) / ND, id = (o - O4) % ND;
+          for (int ib = 0; ib < NB; ++ib)
+            for (int ic = 0; ic < NC; ++ic)
+              s = fma(val[tgt[((ia * NB + ib) * NC + ic) * ND + id]], __ldg(a.D + (bm.bfb + ib) * n + km.bfa + ic), s);
+          dst = a.K + (bm.bfa + ia) * n + km.bfb + id;
+          s *= wk;
+        } else {  // K_bc += sum_ad v D_ad
+          const int ib = (o - O5) / NC, ic = (o - O5) % NC;
+          for (int ia = 0; ia < NA; ++ia)
+            for (int id = 0; id < ND; ++id)
+              s = fma(val[tgt[((ia * NB + ib) * NC + ic) * ND + id]], __ldg(a.D + (bm.bfa + ia) * n + km.bfb + id), s);
+          dst = a.K + (bm.bfb + ib) * n + km.bfa + ic;
+          s *= wk;
+        }
+        atomicAdd(dst, s);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <class C>
+void launch_coop(const CoopTables& tb, const LaunchArgs& a) {
+  const size_t smem = CoopSmem<C>::bytes(tb.nslots);
+  const long long n = a.mode == 0 ? a.nitems : (a.mode == 1 ? a.npair_list : a.nq);
+  if (n <= 0) return;
+  static int blocks_per_sm = 0, sms = 0;
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(coop_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, coop_kernel<C>, C::NT, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const long long cap = static_cast<long long>(blocks_per_sm) * sms;
+  const int grid = a.grid > 0 ? a.grid : static_cast<int>(n < cap ? n : cap);
+  coop_kernel<C><<<grid, C::NT, smem, a.stream>>>(tb, a);
+}
+
+}  // namespace eritile_b200

@@ -21,9 +21,6 @@
 
 namespace eritile_b200 {
 
-#ifndef ERITILE_JK_MINB
-#define ERITILE_JK_MINB 2
-#endif
 
 // Primitive-pair record loads (read-only path). WithPA = false skips the
 // PA/QC half for plans that never read it on that side.
@@ -153,8 +150,8 @@ __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* bo
 
 constexpr int kJkThreads = 256;
 
-template <class C>
-__global__ void __launch_bounds__(kJkThreads, ERITILE_JK_MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
+template <class C, int MINB>
+__global__ void __launch_bounds__(kJkThreads, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
                                                        const PairMeta* __restrict__ pm,
                                                        const PrimRec* __restrict__ prims,
@@ -329,7 +326,9 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
   for (int t = 0; t < C::NV; ++t) out[i * C::NV + t] = v[t];
 }
 
-template <class C>
+// Lane kernels: MINB is the __launch_bounds__ residency target (2 -> up to
+// 128 registers, 3 -> 80); the Workload Allocator picks per class.
+template <class C, int MINB>
 void launch_class(const LaunchArgs& a) {
   const size_t smem = sizeof(double) * kBoysRows * kBoysCols;
   if (a.mode == 0) {
@@ -337,8 +336,8 @@ void launch_class(const LaunchArgs& a) {
     static int blocks_per_sm = 0;
     static int sms = 0;
     if (!blocks_per_sm) {
-      cudaFuncSetAttribute(jk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C>, kJkThreads, smem);
+      cudaFuncSetAttribute(jk_kernel<C, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C, MINB>, kJkThreads, smem);
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -347,7 +346,7 @@ void launch_class(const LaunchArgs& a) {
     const long long want = (a.nitems + (kJkThreads / 32) - 1) / (kJkThreads / 32);
     const long long cap = static_cast<long long>(blocks_per_sm) * sms;
     const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
-    jk_kernel<C><<<grid, kJkThreads, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
+    jk_kernel<C, MINB><<<grid, kJkThreads, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
                                                        a.K, a.N, a.boys_tab);
   } else if (a.mode == 2) {
     if (a.nq <= 0) return;

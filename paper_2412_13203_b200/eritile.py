@@ -82,6 +82,11 @@ def _lib():
         "eritile_gpu_class_profile": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                                 C.c_void_p, C.c_void_p]),
         "eritile_gpu_class_info": (C.c_int, [C.c_int, _ip]),
+        "eritile_gpu_tune": (C.c_int, [C.c_void_p, _dp, C.c_int]),
+        "eritile_gpu_set_variant": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+        "eritile_gpu_get_variant": (C.c_int, [C.c_void_p, C.c_int]),
+        "eritile_gpu_class_nvariants": (C.c_int, [C.c_int]),
+        "eritile_gpu_variant_name": (C.c_char_p, [C.c_int, C.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -281,10 +286,37 @@ class Engine:
         return [dict(cls=tuple(int(v) for v in cls[4 * i:4 * i + 4]), ms=float(ms[i]), flops=float(fl[i]),
                      quartets=int(q[i]), prim_quartets=int(pq[i])) for i in range(n)]
 
+    def tune(self, D: np.ndarray, reps: int = 3) -> "Engine":
+        """Workload Allocator: pick the fastest kernel variant per class on
+        density D."""
+        D = np.ascontiguousarray(D, dtype=np.float64)
+        self._check(self._lib.eritile_gpu_tune(self._h, D, int(reps)))
+        return self
+
+    def set_variant(self, cls_index: int, var) -> "Engine":
+        if isinstance(var, str):
+            var = variant_names(cls_index).index(var)
+        self._check(self._lib.eritile_gpu_set_variant(self._h, int(cls_index), int(var)))
+        return self
+
+    def variants(self) -> dict:
+        """{class (la,lb,lc,ld): chosen variant name}."""
+        out = {}
+        for i, row in enumerate(class_table()):
+            v = self._lib.eritile_gpu_get_variant(self._h, i)
+            out[tuple(int(x) for x in row[:4])] = variant_names(i)[v]
+        return out
+
     def stats(self) -> dict:
         s = Stats()
         self._check(self._lib.eritile_gpu_get_stats(self._h, C.byref(s)))
         return s.as_dict()
+
+
+def variant_names(cls_index: int):
+    lib = _lib()
+    return [lib.eritile_gpu_variant_name(cls_index, v).decode()
+            for v in range(lib.eritile_gpu_class_nvariants(cls_index))]
 
 
 def engine_for(xyz_text: str, basis_text: str, tau: float = 1e-10, device: int = 0,

@@ -150,3 +150,75 @@ def test_dense_reference_loop_water(gpu):
     e = _engine(xyz, bas, 0.0)
     J, K = e.build_jk(D)
     assert np.max(np.abs(J - Jd)) < 1e-10 and np.max(np.abs(K - Kd)) < 1e-10
+
+
+def _force_variant(e, k):
+    """Set every class to its k-th kernel variant (clamped)."""
+    from paper_2412_13203_b200.eritile import class_table, variant_names
+    for i in range(len(class_table())):
+        names = variant_names(i)
+        e.set_variant(i, min(k, len(names) - 1))
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_every_kernel_variant_eri_and_jk(gpu, k):
+    """Every kernel variant (lane_m2 / lane_m3 / coop) of every class gives the
+    oracle's integrals and J/K (benzene 6-31G* covers all L<=2 classes that
+    occur with d shells; water cc-pVDZ the s/p/d mixes)."""
+    for mol, basis, tau in [("benzene", "6-31g*", 1e-12), ("water", "cc-pvdz", 0.0)]:
+        xyz, bas = geom(mol), BASIS[basis]
+        e = _engine(xyz, bas, tau)
+        _force_variant(e, k)
+        O = Oracle("orc").system(xyz, bas)
+        rng = np.random.default_rng(7 + k)
+        n = O.npairs
+        for _ in range(300):
+            x, y = sorted(rng.integers(0, n, 2))
+            g, r = e.eri_quartet(int(x), int(y)), O.eri(int(x), int(y))
+            assert np.allclose(g, r, rtol=1e-12, atol=1e-14), (mol, k, x, y)
+        D = _rand_density(e.nbf, 3)
+        J, K = e.build_jk(D)
+        Jo, Ko, nq = O.build_jk(D, tau)
+        assert nq == e.num_quartets()
+        assert np.max(np.abs(J - Jo)) < 1e-10 and np.max(np.abs(K - Ko)) < 1e-10, (mol, k)
+
+
+def test_tuned_build_matches_oracle(gpu):
+    """The Workload Allocator only picks variants: results stay within 1e-10."""
+    xyz, bas = geom("w4"), BASIS["cc-pvdz"]
+    e = _engine(xyz, bas, 1e-10)
+    D = _rand_density(e.nbf, 4)
+    e.tune(D, reps=1)
+    J, K = e.build_jk(D)
+    Jo, Ko, _ = Oracle("orc").system(xyz, bas).build_jk(D, 1e-10)
+    assert np.max(np.abs(J - Jo)) < 1e-10 and np.max(np.abs(K - Ko)) < 1e-10
+
+
+@pytest.mark.parametrize("kappa", [1e-14, 1e-12])
+def test_kappa_screen_parity(gpu, kappa):
+    """The reference's primitive-pair screen (block.hpp:83-89)
+    applied on both sides: identical lists, J/K within 1e-10; and within 1e-10
+    of the unscreened build as well."""
+    xyz, bas = geom("w4"), BASIS["cc-pvdz"]
+    e = Engine_k(xyz, bas, kappa, 1e-10)
+    O = Oracle("orc").system(xyz, bas, kappa_screen=kappa)
+    assert e.npairs == O.npairs
+    xs, ys = e.quartets()
+    ox, oy = O.quartets(1e-10)
+    order = np.lexsort((oy, ox))
+    assert np.array_equal(xs, ox[order]) and np.array_equal(ys, oy[order])
+    D = _rand_density(e.nbf, 6)
+    J, K = e.build_jk(D)
+    Jo, Ko, _ = O.build_jk(D, 1e-10)
+    assert np.max(np.abs(J - Jo)) < 1e-10 and np.max(np.abs(K - Ko)) < 1e-10
+    if kappa > 1e-14:
+        return
+    J0, K0 = _engine(xyz, bas, 1e-10).build_jk(D)
+    assert np.max(np.abs(J - J0)) < 1e-10 and np.max(np.abs(K - K0)) < 1e-10
+
+
+def Engine_k(xyz, bas, kappa, tau):
+    from paper_2412_13203_b200.eritile import Engine
+    e = Engine(0).load_molecule(xyz, bas).build_pairs(kappa)
+    e.set_screening(tau)
+    return e
