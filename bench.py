@@ -225,9 +225,10 @@ def run_ours(args, rank, nranks, local_rank):
     # before the warm-up builds (untimed, like the reference's tune during
     # the first SCF iterations)
     t1 = time.perf_counter()
-    eng.tune(Dh, reps=3)
+    eng.tune(Dh, reps=2)
     tune_s = time.perf_counter() - t1
     chosen = eng.variants()
+    tune_table = eng.tune_times()
 
     def step():
         eng.build_jk_partial_device(D.data_ptr(), JK.data_ptr(), sp)
@@ -347,6 +348,7 @@ def run_ours(args, rank, nranks, local_rank):
         "clocks": clk.summary(),
         "setup_s": setup_s,
         "tune_s": tune_s,
+        "tune_ms": tune_table,
         "classes": [{"cls": "".join(map(str, r["cls"])), "ms": round(r["ms"], 4),
                      "variant": chosen.get(tuple(r["cls"])),
                      "tflops": r["flops"] / max(r["ms"], 1e-9) / 1e9, "quartets": r["quartets"]}

@@ -35,7 +35,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-co
                   "-I" + str(INCLUDE), "-I" + str(CSRC)]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread", "-I" + str(INCLUDE),
             "-I" + str(CSRC), "-I/usr/local/cuda/include"]
-LMAX = int(os.environ.get("ERITILE_LMAX", "2"))
+LMAX = int(os.environ.get("ERITILE_LMAX", "3"))
 
 
 def _digest(paths, extra: str) -> str:

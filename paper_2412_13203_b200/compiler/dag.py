@@ -22,6 +22,7 @@ emitted plans drive csrc code generation (compiler/emit_cuda.py).
 """
 from __future__ import annotations
 
+import functools
 import heapq
 import random
 from dataclasses import dataclass, field
@@ -319,8 +320,10 @@ def generate_plan(g: DAG, lam: float = 1.0) -> Plan:
                 target_nodes=list(g.targets))
 
 
+@functools.lru_cache(maxsize=None)
 def compile_class(cls, lam: float = 1.0) -> Plan:
-    return generate_plan(build_dag(cls, lam), lam)
+    """Plans are immutable after generation; cached per (class, lambda)."""
+    return generate_plan(build_dag(tuple(cls), lam), lam)
 
 
 def compile_random_class(cls, seed: int) -> Plan:

@@ -61,6 +61,9 @@ PINGPONG_MAX_OPS = int(os.environ.get("ERITILE_PINGPONG", "0"))
 # single-register prefetch of the next bra primitive pair (measured best,
 # profiles/r01_variants.txt)
 PREFETCH = os.environ.get("ERITILE_PREFETCH", "1") == "1"
+# two-ket-primitive variant (eri2) for the smallest plans
+UNROLL2 = True
+UNROLL2_MAX_OPS = 60
 
 
 def _coef_expr(kind: int, d: int, side_swap: bool) -> str:
@@ -172,6 +175,52 @@ def emit_class(cls) -> Tuple[str, Dict]:
     btext = "\n".join(body)
     bload = "load_prim<%s>" % ("true" if "bPA" in btext else "false")
     kload = "load_prim<%s>" % ("true" if "kPA" in btext else "false")
+    def emit_eri2():
+        """Two ket primitives per step: bodies A (t) and B (u) share the bra
+        record; u is folded into t after the loop. Odd kk: tail with A."""
+        w("  __device__ __forceinline__ static void eri2(")
+        w("      const PrimRec* __restrict__ bra, int kb, const PrimRec* __restrict__ ket, int kk,")
+        w("      double ABx, double ABy, double ABz, double CDx, double CDy, double CDz,")
+        w("      const double* __restrict__ btab, double (&out)[NV]) {")
+        for n, t in bnd_name.items():
+            w(f"    double {t} = 0.0, u{t[1:]} = 0.0;")
+        bodyB = []
+        for ln in body:
+            for n in plan.boundary:
+                pre = bnd_name[n] + " += "
+                if ln.startswith(pre):
+                    ln = "u" + bnd_name[n][1:] + " += " + ln[len(pre):]
+                    break
+            bodyB.append(ln)
+        w("    int j = 0;")
+        w("    for (; j + 1 < kk; j += 2) {")
+        w(f"      const PrimRec k0 = {kload}(ket + j);")
+        w(f"      const PrimRec k1 = {kload}(ket + j + 1);")
+        w(f"      PrimRec bn = {bload}(bra);")
+        w("      for (int i = 0; i < kb; ++i) {")
+        w("        const PrimRec bq = bn;")
+        w(f"        bn = {bload}(bra + (i + 1 < kb ? i + 1 : i));")
+        for var, bd in (("k0", body), ("k1", bodyB)):
+            w("        {")
+            w("          const PrimRec& bp = bq;")
+            w(f"          const PrimRec& kp = {var};")
+            for ln in bd:
+                w("          " + ln)
+            w("        }")
+        w("      }")
+        w("    }")
+        w("    if (j < kk) {")
+        w(f"      const PrimRec kp = {kload}(ket + j);")
+        w("      for (int i = 0; i < kb; ++i) {")
+        w(f"        const PrimRec bq = {bload}(bra + i);")
+        emit_body("bq", "        ")
+        w("      }")
+        w("    }")
+        for n, t in bnd_name.items():
+            w(f"    {t} += u{t[1:]};")
+        emit_tail()
+        w("  }")
+
     w("    for (int j = 0; j < kk; ++j) {")
     w(f"      const PrimRec kp = {kload}(ket + j);")
     if pingpong:
@@ -201,30 +250,35 @@ def emit_class(cls) -> Tuple[str, Dict]:
         emit_body("bq", "        ")
         w("      }")
     w("    }")
-    # contracted segment
-    for n in plan.upper_order:
-        expr = None
-        for t in plan.deriv[n]:
-            c = _coef_expr(t.kind, t.dir, swap)
-            src = val_after_contract(t.node)
-            if t.kind == UNIT and t.factor == 1.0:
-                expr = src if expr is None else f"({expr} + {src})"
-            else:
-                if t.factor != 1.0:
-                    c = f"({_fmt_factor(t.factor)} * {c})"
-                expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
-        w(f"    const double {upper_name[n]} = {expr};")
-    # targets: map kernel a-major (a,b,c,d) -> plan node
-    ca, cb, cc, cd = (components(L) for L in cls)
-    k = 0
-    for a in ca:
-        for b in cb:
-            for c in cc:
-                for d in cd:
-                    node = (c, d, a, b, 0) if swap else (a, b, c, d, 0)
-                    w(f"    out[{k}] = {val_after_contract(node)};")
-                    k += 1
+
+    def emit_tail():
+        # contracted segment
+        for n in plan.upper_order:
+            expr = None
+            for t in plan.deriv[n]:
+                c = _coef_expr(t.kind, t.dir, swap)
+                src = val_after_contract(t.node)
+                if t.kind == UNIT and t.factor == 1.0:
+                    expr = src if expr is None else f"({expr} + {src})"
+                else:
+                    if t.factor != 1.0:
+                        c = f"({_fmt_factor(t.factor)} * {c})"
+                    expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
+            w(f"    const double {upper_name[n]} = {expr};")
+        # targets: map kernel a-major (a,b,c,d) -> plan node
+        ca, cb, cc, cd = (components(L) for L in cls)
+        k = 0
+        for a in ca:
+            for b in cb:
+                for c in cc:
+                    for d in cd:
+                        node = (c, d, a, b, 0) if swap else (a, b, c, d, 0)
+                        w(f"    out[{k}] = {val_after_contract(node)};")
+                        k += 1
+    emit_tail()
     w("  }")
+    if UNROLL2 and plan.op_count <= UNROLL2_MAX_OPS:
+        emit_eri2()
     w("};")
     info = dict(cls=cls, swap=swap, ops=plan.op_count, M=M, nv=na * nb * nc * nd,
                 boundary=len(plan.boundary), prim_terms=sum(len(i.terms) for i in plan.prim if i.base_m < 0),
@@ -242,6 +296,7 @@ LANE_MAX_OPS = int(os.environ.get("ERITILE_LANE_MAX_OPS", "4000"))
 COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2, 3)
+COOP_SMEM_BUDGET = 110 * 1024  # keep >= 2 CTAs/SM when the Boys slice is staged
 
 
 def variants(info) -> List[Tuple[str, str]]:
@@ -252,6 +307,14 @@ def variants(info) -> List[Tuple[str, str]]:
         mins = MINB_VARIANTS if info["ops"] <= MINB_SMALL_OPS else (2,)
         for m in mins:
             out.append((f"lane_m{m}", f"launch_class<Cls{cid}, {m}>"))
+        if info["ops"] <= MINB_SMALL_OPS:
+            # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads
+            out.append(("lane_t512", f"launch_class<Cls{cid}, 1, 1, 512>"))
+            out.append(("lane_t768", f"launch_class<Cls{cid}, 1, 1, 768>"))
+        if UNROLL2 and info["ops"] <= UNROLL2_MAX_OPS:
+            for m in mins:
+                out.append((f"lane_u2m{m}", f"launch_class<Cls{cid}, {m}, 2>"))
+            out.append(("lane_u2t512", f"launch_class<Cls{cid}, 1, 2, 512>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
     return out
@@ -294,7 +357,12 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
             width = max(b - a for a, b in zip(sc["lo_lvl"], sc["lo_lvl"][1:]))
             nt = 256 if width >= 192 else 128
             src.append(emit_tables(cid, sc))
-            src.append(f"struct CoopCls{cid} : Cls{cid} {{ static constexpr int NT = {nt}; }};")
+            na, nb_, nc, nd = map(ncart, cls)
+            need = 8 * (48 + 64 + sc["nslots"]) + 2 * na * nb_ * nc * nd
+            boys_smem = need + 8 * 641 * 10 <= COOP_SMEM_BUDGET
+            assert need <= 227 * 1024, (cls, need)
+            src.append(f"struct CoopCls{cid} : Cls{cid} {{ static constexpr int NT = {nt}; "
+                       f"static constexpr bool BOYS_SMEM = {'true' if boys_smem else 'false'}; }};")
             src.append(f"void launch_coop_cls{cid}(const LaunchArgs& a) {{")
             src.append("  CoopTables t{};")
             for fld, sym in [("lo", "kLo"), ("lo_lvl", "kLoLvl"), ("bd", "kBd"), ("up", "kUp"),
@@ -323,8 +391,8 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         la, lb, lc, ld = info["cls"]
         cid = class_id(info["cls"])
         vs = info["variants"]
-        fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (4 - len(vs))
-        names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (4 - len(vs))
+        fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (8 - len(vs))
+        names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (8 - len(vs))
         reg.append(f"  {{{la}, {lb}, {lc}, {ld}, {info['M']}, {info['ops']}, {info['prim_terms']}, "
                    f"{info['base']}, {info['contract']}, {info['hrr_terms']}, {len(vs)}, {{{fns}}}, "
                    f"{{{names}}}, {info['default']}}},")

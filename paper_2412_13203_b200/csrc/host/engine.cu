@@ -227,7 +227,7 @@ struct eritile_gpu {
 
   // Workload Allocator state: kernel variant per class (kClassTable[c].var)
   std::vector<int> var_choice;
-  std::vector<double> tune_ms;  // per class launch: best measured ms (tune)
+  std::vector<double> tune_ms;  // per class launch x kMaxVariants: median ms (tune)
 
   bool profiling = false;
   bool host_only = false;  // device < 0: block constructor / lists only
@@ -261,7 +261,7 @@ struct eritile_gpu {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    tune_ms.assign(work.size(), 0.0);
+    tune_ms.assign(work.size() * kMaxVariants, 0.0);
     for (size_t w = 0; w < work.size(); ++w) {
       const ClassWork& cw = work[w];
       const ClassEntry& ce = kClassTable[cw.cls];
@@ -280,13 +280,13 @@ struct eritile_gpu {
         }
         std::sort(t.begin(), t.end());
         const double med = t[t.size() / 2];
+        tune_ms[w * kMaxVariants + v] = med;
         if (med < best) {
           best = med;
           bestv = v;
         }
       }
       var_choice[cw.cls] = bestv;
-      tune_ms[w] = best;
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1091,6 +1091,18 @@ int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps) {
     ctx->prescale(ctx->d_D.p, ctx->d_Ds.p, ctx->stream);
     ctx->tune(ctx->d_Ds.p, reps);
   });
+}
+
+int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  const int n = static_cast<int>(ctx->work.size());
+  if (ctx->tune_ms.size() != ctx->work.size() * kMaxVariants) return 0;
+  for (int w = 0; w < std::min(n, cap); ++w) {
+    if (cls_index) cls_index[w] = ctx->work[w].cls;
+    if (ms)
+      for (int v = 0; v < kMaxVariants; ++v) ms[w * kMaxVariants + v] = ctx->tune_ms[w * kMaxVariants + v];
+  }
+  return n;
 }
 
 int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var) {

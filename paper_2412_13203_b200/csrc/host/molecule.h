@@ -9,7 +9,7 @@
 namespace eritile_b200 {
 
 constexpr double kAngstromToBohr = 1.8897259886;  // molecule.hpp:16
-constexpr int kMaxShellL = 2;                      // classes generated up to (dd|dd)
+constexpr int kMaxShellL = 4;  // parser + one-electron bound; ERI classes: kMaxL (registry)
 
 struct InputError : std::runtime_error {
   explicit InputError(const std::string& m) : std::runtime_error(m) {}

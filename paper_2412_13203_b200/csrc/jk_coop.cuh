@@ -35,9 +35,11 @@ struct CoopTables {
   int nslots;
 };
 
+// C::BOYS_SMEM: stage the class's Boys slice in shared memory (51 KB) or read
+// it through L1 from global memory (classes whose value slots need the room).
 template <class C>
 struct CoopSmem {
-  static constexpr size_t boys = sizeof(double) * kBoysRows * kBoysCols;
+  static constexpr size_t boys = C::BOYS_SMEM ? sizeof(double) * kBoysRows * kBoysCols : 0;
   static size_t bytes(int nslots) {
     return boys + sizeof(double) * (kCoopBase + kCoopMaxCombo + nslots) +
            ((sizeof(unsigned short) * C::NV + 15) & ~size_t(15));
@@ -137,12 +139,12 @@ __device__ __forceinline__ void coop_eval(const CoopTables& tb, const PairMeta& 
 template <class C>
 __global__ void __launch_bounds__(C::NT) coop_kernel(CoopTables tb, LaunchArgs a) {
   extern __shared__ __align__(16) double smem[];
-  double* s_boys = smem;
-  double* coefb = s_boys + kBoysRows * kBoysCols;
+  const double* s_boys = C::BOYS_SMEM ? smem : a.boys_tab + static_cast<size_t>(C::M) * kBoysRows * kBoysCols;
+  double* coefb = smem + (C::BOYS_SMEM ? kBoysRows * kBoysCols : 0);
   double* cf = coefb + kCoopBase;
   double* val = cf + kCoopMaxCombo;
   unsigned short* tgt = reinterpret_cast<unsigned short*>(val + tb.nslots);
-  load_boys_slice(s_boys, a.boys_tab, C::M);
+  if (C::BOYS_SMEM) load_boys_slice(smem, a.boys_tab, C::M);
   for (int k = threadIdx.x; k < C::NV; k += C::NT) tgt[k] = __ldg(tb.tgt + k);
   if (threadIdx.x == 0) val[0] = 1.0;
   __syncthreads();

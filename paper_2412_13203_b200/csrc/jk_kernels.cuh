@@ -150,8 +150,10 @@ __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* bo
 
 constexpr int kJkThreads = 256;
 
-template <class C, int MINB>
-__global__ void __launch_bounds__(kJkThreads, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
+// U = 1: C::eri (one primitive quartet per step); U = 2: C::eri2 (two ket
+// primitives per step sharing the bra record, two independent FMA chains).
+template <class C, int MINB, int U = 1, int NT = kJkThreads>
+__global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
                                                        const PairMeta* __restrict__ pm,
                                                        const PrimRec* __restrict__ prims,
@@ -180,8 +182,12 @@ __global__ void __launch_bounds__(kJkThreads, MINB) jk_kernel(const WorkItem* __
     const PairMeta bm = pm[x];
     const PairMeta km = pm[y];
     double v[C::NV];
-    C::eri(prims + bm.prim_off, bm.K, prims + km.prim_off, active ? km.K : 0, bm.ABx, bm.ABy, bm.ABz,
-           km.ABx, km.ABy, km.ABz, s_boys, v);
+    if constexpr (U == 2)
+      C::eri2(prims + bm.prim_off, bm.K, prims + km.prim_off, active ? km.K : 0, bm.ABx, bm.ABy, bm.ABz,
+              km.ABx, km.ABy, km.ABz, s_boys, v);
+    else
+      C::eri(prims + bm.prim_off, bm.K, prims + km.prim_off, active ? km.K : 0, bm.ABx, bm.ABy, bm.ABz,
+             km.ABx, km.ABy, km.ABz, s_boys, v);
     const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (x != y ? 2.0 : 1.0);
     const double wj = active ? 0.5 * deg : 0.0;
     const double wk = active ? 0.25 * deg : 0.0;
@@ -328,7 +334,10 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 
 // Lane kernels: MINB is the __launch_bounds__ residency target (2 -> up to
 // 128 registers, 3 -> 80); the Workload Allocator picks per class.
-template <class C, int MINB>
+// NT: threads per CTA. One Boys slice is staged per CTA, so 512/768-thread
+// CTAs at MINB = 1 keep 16/24 warps per SM with a single 51 KB table and
+// leave the rest of the 256 KB L1/shared array to L1 (primitive records).
+template <class C, int MINB, int U = 1, int NT = kJkThreads>
 void launch_class(const LaunchArgs& a) {
   const size_t smem = sizeof(double) * kBoysRows * kBoysCols;
   if (a.mode == 0) {
@@ -336,17 +345,17 @@ void launch_class(const LaunchArgs& a) {
     static int blocks_per_sm = 0;
     static int sms = 0;
     if (!blocks_per_sm) {
-      cudaFuncSetAttribute(jk_kernel<C, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C, MINB>, kJkThreads, smem);
+      cudaFuncSetAttribute(jk_kernel<C, MINB, U, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C, MINB, U, NT>, NT, smem);
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    const long long want = (a.nitems + (kJkThreads / 32) - 1) / (kJkThreads / 32);
+    const long long want = (a.nitems + (NT / 32) - 1) / (NT / 32);
     const long long cap = static_cast<long long>(blocks_per_sm) * sms;
     const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
-    jk_kernel<C, MINB><<<grid, kJkThreads, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
+    jk_kernel<C, MINB, U, NT><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
                                                        a.K, a.N, a.boys_tab);
   } else if (a.mode == 2) {
     if (a.nq <= 0) return;

@@ -84,6 +84,7 @@ def _lib():
         "eritile_gpu_class_info": (C.c_int, [C.c_int, _ip]),
         "eritile_gpu_tune": (C.c_int, [C.c_void_p, _dp, C.c_int]),
         "eritile_gpu_set_variant": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+        "eritile_gpu_tune_times": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
         "eritile_gpu_get_variant": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_class_nvariants": (C.c_int, [C.c_int]),
         "eritile_gpu_variant_name": (C.c_char_p, [C.c_int, C.c_int]),
@@ -298,6 +299,19 @@ class Engine:
             var = variant_names(cls_index).index(var)
         self._check(self._lib.eritile_gpu_set_variant(self._h, int(cls_index), int(var)))
         return self
+
+    def tune_times(self) -> dict:
+        """{class: {variant name: median ms}} of the last tune."""
+        n = self._lib.eritile_gpu_tune_times(self._h, 0, None, None)
+        ci = np.zeros(max(n, 1), np.int32)
+        ms = np.zeros(8 * max(n, 1))
+        self._lib.eritile_gpu_tune_times(self._h, n, ci.ctypes.data, ms.ctypes.data)
+        tab = class_table()
+        out = {}
+        for w in range(n):
+            names = variant_names(int(ci[w]))
+            out["".join(map(str, tab[ci[w]][:4]))] = {nm: round(float(ms[8 * w + v]), 4) for v, nm in enumerate(names)}
+        return out
 
     def variants(self) -> dict:
         """{class (la,lb,lc,ld): chosen variant name}."""

@@ -44,9 +44,16 @@ def test_create_without_gpu_fails_loudly():
 
 def test_class_table():
     from paper_2412_13203_b200.eritile import class_table
+    from paper_2412_13203_b200.eritile import variant_names
     t = class_table()
-    assert len(t) == 21  # canonical classes for L <= 2
+    assert len(t) == 55  # canonical classes for L <= 3 (La>=Lb, Lc>=Ld, bra key >= ket key)
     assert t[0][:4] == (0, 0, 0, 0)
+    assert {r[:4] for r in t} >= {(3, 3, 3, 3), (2, 2, 2, 2), (3, 0, 1, 0)}
+    for i, r in enumerate(t):  # every class has >= 1 kernel; coop for the big plans
+        names = variant_names(i)
+        assert names and len(set(names)) == len(names)
+        if r[5] > 4000:
+            assert names == ["coop"]
 
 
 @pytest.mark.parametrize("mol,basis", [("water", "sto-3g"), ("benzene", "6-31g*"), ("w8", "cc-pvdz")])

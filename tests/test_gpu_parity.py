@@ -160,7 +160,7 @@ def _force_variant(e, k):
         e.set_variant(i, min(k, len(names) - 1))
 
 
-@pytest.mark.parametrize("k", [0, 1, 2])
+@pytest.mark.parametrize("k", list(range(8)))
 def test_every_kernel_variant_eri_and_jk(gpu, k):
     """Every kernel variant (lane_m2 / lane_m3 / coop) of every class gives the
     oracle's integrals and J/K (benzene 6-31G* covers all L<=2 classes that
@@ -222,3 +222,25 @@ def Engine_k(xyz, bas, kappa, tau):
     e = Engine(0).load_molecule(xyz, bas).build_pairs(kappa)
     e.set_screening(tau)
     return e
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_f_shells_cc_pvtz(gpu, k):
+    """L=3 (f) classes: water/cc-pVTZ integrals and J/K vs the oracle, for the
+    default and the alternative kernel variant of every class."""
+    xyz, bas = geom("water"), BASIS["cc-pvtz"]
+    e = _engine(xyz, bas, 1e-12)
+    if k:
+        _force_variant(e, 9)
+    O = Oracle("orc").system(xyz, bas)
+    rng = np.random.default_rng(11)
+    n = O.npairs
+    for _ in range(400):
+        x, y = sorted(rng.integers(0, n, 2))
+        g, r = e.eri_quartet(int(x), int(y)), O.eri(int(x), int(y))
+        assert np.allclose(g, r, rtol=1e-12, atol=1e-13), (x, y, np.max(np.abs(g - r)))
+    D = _rand_density(e.nbf, 12)
+    J, K = e.build_jk(D)
+    Jo, Ko, nq = O.build_jk(D, 1e-12)
+    assert nq == e.num_quartets()
+    assert np.max(np.abs(J - Jo)) < 1e-10 and np.max(np.abs(K - Ko)) < 1e-10

@@ -17,7 +17,8 @@ def _oracle_scf(mol, basis, tau):
 
 
 @pytest.mark.parametrize("mol,basis,tau", [("water", "sto-3g", 0.0), ("water", "cc-pvdz", 1e-12),
-                                           ("benzene", "6-31g*", 1e-12), ("w4", "cc-pvdz", 1e-10)])
+                                           ("benzene", "6-31g*", 1e-12), ("w4", "cc-pvdz", 1e-10),
+                                           ("water", "cc-pvtz", 1e-12)])
 def test_scf_energy_vs_oracle(gpu, mol, basis, tau):
     from paper_2412_13203_b200.scf import run_rhf
     g = run_rhf(geom(mol), BASIS[basis], tau=tau, conv=1e-9, e_conv=1e-12)

@@ -19,13 +19,18 @@ ap.add_argument("--waters", type=int, default=16)
 ap.add_argument("--basis", default="cc-pvdz.txt")
 ap.add_argument("--tau", type=float, default=1e-10)
 ap.add_argument("--builds", type=int, default=2)
+ap.add_argument("--kappa", type=float, default=1e-14)
+ap.add_argument("--tune", action="store_true")
 a = ap.parse_args()
-e = Engine(0).load_molecule(water_cluster(a.waters), read_fixture("basis", a.basis)).build_pairs(0.0)
+e = Engine(0).load_molecule(water_cluster(a.waters), read_fixture("basis", a.basis)).build_pairs(a.kappa)
 e.set_screening(a.tau)
 N = e.nbf
 rng = np.random.default_rng(0)
 C, _ = np.linalg.qr(rng.standard_normal((N, e.nelectrons // 2)))
 D = C @ C.T
+if a.tune:
+    e.tune(D, reps=1)
+    print(e.variants())
 for _ in range(a.builds):
     J, K = e.build_jk(D)
 print(e.stats())
