@@ -137,7 +137,7 @@ int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, 
  * level-scheduled plan). The choice changes atomic summation order only. */
 int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps);
 /* Per class launch of the last tune: class table index and the median ms of
- * each variant (kMaxVariants = 8 per launch, 0 = no such variant). */
+ * each variant (kMaxVariants = 12 per launch, 0 = no such variant). */
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms);
 int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var);
 int eritile_gpu_get_variant(const eritile_gpu* ctx, int cls_index);

@@ -32,7 +32,7 @@ INCLUDE = ROOT / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
-                  "-I" + str(INCLUDE), "-I" + str(CSRC)]
+                  "-I" + str(INCLUDE), "-I" + str(CSRC)] + os.environ.get("ERITILE_NVFLAGS", "").split()
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread", "-I" + str(INCLUDE),
             "-I" + str(CSRC), "-I/usr/local/cuda/include"]
 LMAX = int(os.environ.get("ERITILE_LMAX", "3"))
@@ -84,6 +84,9 @@ def build(jobs: int | None = None, verbose: bool = True) -> Path:
     jobs = jobs or max(2, os.cpu_count() or 2)
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(lambda u: _compile(*u), units))
+    for stale in OBJ.glob("*.o"):  # objects of superseded sources
+        if stale not in objs:
+            stale.unlink()
     key = _digest(objs, "link")
     stamp = LIBDIR / (".link." + LIB.name)
     if LIB.exists() and stamp.exists() and stamp.read_text() == key:

@@ -55,14 +55,7 @@ def ncart(L: int) -> int:
 
 
 DIRS = "xyz"
-# classes with at most this many plan operations get the two-register
-# ping-pong primitive loop (body emitted twice); larger ones a plain loop
-PINGPONG_MAX_OPS = int(os.environ.get("ERITILE_PINGPONG", "0"))
-# single-register prefetch of the next bra primitive pair (measured best,
-# profiles/r01_variants.txt)
-PREFETCH = os.environ.get("ERITILE_PREFETCH", "1") == "1"
-# two-ket-primitive variant (eri2) for the smallest plans
-UNROLL2 = True
+# the two-ket loop variant only for the smallest plans (register budget)
 UNROLL2_MAX_OPS = 60
 
 
@@ -88,6 +81,16 @@ def _fmt_factor(f: float) -> str:
 
 
 def emit_class(cls) -> Tuple[str, Dict]:
+    """Straight-line pieces of one class for the lane kernels.
+
+    ``prim(bp, kp, btab, acc)`` is one primitive quartet: binding
+    (SPEC.md:290,316), Boys, the plan's vertical segment, fold into the
+    contracted accumulators ``acc`` (compiler.hpp:141-143). ``finish(acc, AB,
+    CD, out)`` is the horizontal segment and the a-major targets
+    (compiler.hpp:144-145, dag.hpp:221-229). The primitive loop nests that
+    drive them (plain, prefetching, two-ket, ping-pong) are C++ templates in
+    csrc/jk_kernels.cuh, so loop structure is a kernel variant, not codegen.
+    """
     la, lb, lc, ld = cls
     p_fwd = compile_class(cls)
     p_swp = compile_class((lc, ld, la, lb))
@@ -99,7 +102,6 @@ def emit_class(cls) -> Tuple[str, Dict]:
 
     lines: List[str] = []
     w = lines.append
-    # names for nodes
     lower_name = {n: f"r{i}" for i, n in enumerate(plan.lower_order)}
     bnd_name = {n: f"t{i}" for i, n in enumerate(plan.boundary)}
     upper_name = {n: f"h{i}" for i, n in enumerate(plan.upper_order)}
@@ -109,23 +111,6 @@ def emit_class(cls) -> Tuple[str, Dict]:
             return upper_name[n]
         return bnd_name[n]
 
-    w(f"// ERI class ({la},{lb},{lc},{ld}); plan orientation "
-      f"{'(ket|bra)' if swap else '(bra|ket)'}; ops {plan.op_count}; "
-      f"boundary {len(plan.boundary)}; max_m {M}")
-    w(f"struct Cls{cid} {{")
-    w(f"  static constexpr int LA = {la}, LB = {lb}, LC = {lc}, LD = {ld};")
-    w(f"  static constexpr int NA = {na}, NB = {nb}, NC = {nc}, ND = {nd};")
-    w(f"  static constexpr int NV = {na * nb * nc * nd};")
-    w(f"  static constexpr int M = {M};")
-    w(f"  static constexpr int OPS = {plan.op_count};")
-    w("  __device__ __forceinline__ static void eri(")
-    w("      const PrimRec* __restrict__ bra, int kb, const PrimRec* __restrict__ ket, int kk,")
-    w("      double ABx, double ABy, double ABz, double CDx, double CDy, double CDz,")
-    w("      const double* __restrict__ btab, double (&out)[NV]) {")
-    for n, t in bnd_name.items():
-        w(f"    double {t} = 0.0;")
-    # Per-primitive-quartet body: binding, Boys, the plan's
-    # primitive segment, fold into the contracted accumulators.
     body: List[str] = []
     b = body.append
     b("const double pq = bp.p + kp.p;")
@@ -161,124 +146,68 @@ def emit_class(cls) -> Tuple[str, Dict]:
                 c = f"({_fmt_factor(t.factor)} * {c})"
             expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
         b(f"const double {nm} = {expr};")
+    nhead = len(body)
     for n in plan.boundary:
-        b(f"{bnd_name[n]} += {lower_name[n]};")
+        b(f"a.{bnd_name[n]} += {lower_name[n]};")
+    btext = "\n".join(body[nhead - len(plan.boundary) - len([x for x in plan.lower_order]):])
+    optext = "\n".join(ln for ln in body if ln.startswith("const double r"))
 
-    def emit_body(var: str, indent: str):
-        w(indent + "{")
-        w(indent + f"  const PrimRec& bp = {var};")
-        for ln in body:
-            w(indent + "  " + ln)
-        w(indent + "}")
-
-    pingpong = plan.op_count <= PINGPONG_MAX_OPS
-    btext = "\n".join(body)
-    bload = "load_prim<%s>" % ("true" if "bPA" in btext else "false")
-    kload = "load_prim<%s>" % ("true" if "kPA" in btext else "false")
-    def emit_eri2():
-        """Two ket primitives per step: bodies A (t) and B (u) share the bra
-        record; u is folded into t after the loop. Odd kk: tail with A."""
-        w("  __device__ __forceinline__ static void eri2(")
-        w("      const PrimRec* __restrict__ bra, int kb, const PrimRec* __restrict__ ket, int kk,")
-        w("      double ABx, double ABy, double ABz, double CDx, double CDy, double CDz,")
-        w("      const double* __restrict__ btab, double (&out)[NV]) {")
-        for n, t in bnd_name.items():
-            w(f"    double {t} = 0.0, u{t[1:]} = 0.0;")
-        bodyB = []
-        for ln in body:
-            for n in plan.boundary:
-                pre = bnd_name[n] + " += "
-                if ln.startswith(pre):
-                    ln = "u" + bnd_name[n][1:] + " += " + ln[len(pre):]
-                    break
-            bodyB.append(ln)
-        w("    int j = 0;")
-        w("    for (; j + 1 < kk; j += 2) {")
-        w(f"      const PrimRec k0 = {kload}(ket + j);")
-        w(f"      const PrimRec k1 = {kload}(ket + j + 1);")
-        w(f"      PrimRec bn = {bload}(bra);")
-        w("      for (int i = 0; i < kb; ++i) {")
-        w("        const PrimRec bq = bn;")
-        w(f"        bn = {bload}(bra + (i + 1 < kb ? i + 1 : i));")
-        for var, bd in (("k0", body), ("k1", bodyB)):
-            w("        {")
-            w("          const PrimRec& bp = bq;")
-            w(f"          const PrimRec& kp = {var};")
-            for ln in bd:
-                w("          " + ln)
-            w("        }")
-        w("      }")
-        w("    }")
-        w("    if (j < kk) {")
-        w(f"      const PrimRec kp = {kload}(ket + j);")
-        w("      for (int i = 0; i < kb; ++i) {")
-        w(f"        const PrimRec bq = {bload}(bra + i);")
-        emit_body("bq", "        ")
-        w("      }")
-        w("    }")
-        for n, t in bnd_name.items():
-            w(f"    {t} += u{t[1:]};")
-        emit_tail()
-        w("  }")
-
-    w("    for (int j = 0; j < kk; ++j) {")
-    w(f"      const PrimRec kp = {kload}(ket + j);")
-    if pingpong:
-        # software pipelining without register copies: two primitive-pair
-        # registers b0/b1 alternate, each reloaded (clamped, branch-free)
-        # right after its last use, so L1 latency hides behind a full body
-        w(f"      PrimRec b0 = {bload}(bra);")
-        w(f"      PrimRec b1 = {bload}(bra + (kb > 1 ? 1 : 0));")
-        w("      for (int i = 0; i < kb; i += 2) {")
-        emit_body("b0", "        ")
-        w(f"        b0 = {bload}(bra + (i + 2 < kb ? i + 2 : kb - 1));")
-        w("        if (i + 1 < kb) {")
-        emit_body("b1", "          ")
-        w("        }")
-        w(f"        b1 = {bload}(bra + (i + 3 < kb ? i + 3 : kb - 1));")
-        w("      }")
-    elif PREFETCH:
-        w(f"      PrimRec bn = {bload}(bra);")
-        w("      for (int i = 0; i < kb; ++i) {")
-        w("        const PrimRec bq = bn;")
-        w(f"        bn = {bload}(bra + (i + 1 < kb ? i + 1 : i));")
-        emit_body("bq", "        ")
-        w("      }")
-    else:
-        w("      for (int i = 0; i < kb; ++i) {")
-        w(f"        const PrimRec bq = {bload}(bra + i);")
-        emit_body("bq", "        ")
-        w("      }")
-    w("    }")
-
-    def emit_tail():
-        # contracted segment
-        for n in plan.upper_order:
-            expr = None
-            for t in plan.deriv[n]:
-                c = _coef_expr(t.kind, t.dir, swap)
-                src = val_after_contract(t.node)
-                if t.kind == UNIT and t.factor == 1.0:
-                    expr = src if expr is None else f"({expr} + {src})"
-                else:
-                    if t.factor != 1.0:
-                        c = f"({_fmt_factor(t.factor)} * {c})"
-                    expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
-            w(f"    const double {upper_name[n]} = {expr};")
-        # targets: map kernel a-major (a,b,c,d) -> plan node
-        ca, cb, cc, cd = (components(L) for L in cls)
-        k = 0
-        for a in ca:
-            for b in cb:
-                for c in cc:
-                    for d in cd:
-                        node = (c, d, a, b, 0) if swap else (a, b, c, d, 0)
-                        w(f"    out[{k}] = {val_after_contract(node)};")
-                        k += 1
-    emit_tail()
+    w(f"// ERI class ({la},{lb},{lc},{ld}); plan orientation "
+      f"{'(ket|bra)' if swap else '(bra|ket)'}; ops {plan.op_count}; "
+      f"boundary {len(plan.boundary)}; max_m {M}")
+    w(f"struct Cls{cid} {{")
+    w(f"  static constexpr int LA = {la}, LB = {lb}, LC = {lc}, LD = {ld};")
+    w(f"  static constexpr int NA = {na}, NB = {nb}, NC = {nc}, ND = {nd};")
+    w(f"  static constexpr int NV = {na * nb * nc * nd};")
+    w(f"  static constexpr int M = {M};")
+    w(f"  static constexpr int OPS = {plan.op_count};")
+    w(f"  static constexpr bool BPA = {'true' if 'bPA' in optext else 'false'};  // plan reads bra PA")
+    w(f"  static constexpr bool KPA = {'true' if 'kPA' in optext else 'false'};  // plan reads ket PA (QC)")
+    w("  struct Acc { double " + ", ".join(bnd_name[n] for n in plan.boundary) + "; };")
+    w("  __device__ __forceinline__ static void zero(Acc& a) {")
+    w("    " + " ".join(f"a.{bnd_name[n]} = 0.0;" for n in plan.boundary))
     w("  }")
-    if UNROLL2 and plan.op_count <= UNROLL2_MAX_OPS:
-        emit_eri2()
+    w("  __device__ __forceinline__ static void fold(Acc& a, const Acc& b) {")
+    w("    " + " ".join(f"a.{bnd_name[n]} += b.{bnd_name[n]};" for n in plan.boundary))
+    w("  }")
+    w("  __device__ __forceinline__ static void prim(const PrimRec& bp, const PrimRec& kp,")
+    w("                                              const double* __restrict__ btab, Acc& a) {")
+    for ln in body:
+        w("    " + ln)
+    w("  }")
+    w("  __device__ __forceinline__ static void finish(const Acc& a, double ABx, double ABy, double ABz,")
+    w("                                                double CDx, double CDy, double CDz, double (&out)[NV]) {")
+    w("    (void)ABx; (void)ABy; (void)ABz; (void)CDx; (void)CDy; (void)CDz;")
+    for n in plan.boundary:
+        w(f"    const double {bnd_name[n]} = a.{bnd_name[n]};")
+    for n in plan.upper_order:
+        expr = None
+        for t in plan.deriv[n]:
+            c = _coef_expr(t.kind, t.dir, swap)
+            src = val_after_contract(t.node)
+            if t.kind == UNIT and t.factor == 1.0:
+                expr = src if expr is None else f"({expr} + {src})"
+            else:
+                if t.factor != 1.0:
+                    c = f"({_fmt_factor(t.factor)} * {c})"
+                expr = f"{c} * {src}" if expr is None else f"fma({c}, {src}, {expr})"
+        w(f"    const double {upper_name[n]} = {expr};")
+    ca, cb, cc, cd = (components(L) for L in cls)
+    k = 0
+    for a in ca:
+        for b_ in cb:
+            for c in cc:
+                for d in cd:
+                    node = (c, d, a, b_, 0) if swap else (a, b_, c, d, 0)
+                    w(f"    out[{k}] = {val_after_contract(node)};")
+                    k += 1
+    w("  }")
+    w("  __device__ __forceinline__ static void eri(")
+    w("      const PrimRec* __restrict__ bra, int kb, const PrimRec* __restrict__ ket, int kk,")
+    w("      double ABx, double ABy, double ABz, double CDx, double CDy, double CDz,")
+    w("      const double* __restrict__ btab, double (&out)[NV]) {")
+    w(f"    eri_drive<Cls{cid}, kLoopPrefetch>(bra, kb, ket, kk, ABx, ABy, ABz, CDx, CDy, CDz, btab, out);")
+    w("  }")
     w("};")
     info = dict(cls=cls, swap=swap, ops=plan.op_count, M=M, nv=na * nb * nc * nd,
                 boundary=len(plan.boundary), prim_terms=sum(len(i.terms) for i in plan.prim if i.base_m < 0),
@@ -306,17 +235,24 @@ def variants(info) -> List[Tuple[str, str]]:
     if info["ops"] <= LANE_MAX_OPS:
         mins = MINB_VARIANTS if info["ops"] <= MINB_SMALL_OPS else (2,)
         for m in mins:
-            out.append((f"lane_m{m}", f"launch_class<Cls{cid}, {m}>"))
+            out.append((f"lane_m{m}", f"launch_class<Cls{cid}, {m}, kLoopPrefetch>"))
+        if info["ops"] > MINB_SMALL_OPS:
+            out.append(("lane_plm2", f"launch_class<Cls{cid}, 2, kLoopPlain>"))
+            out.append(("lane_sbm2", f"launch_class<Cls{cid}, 2, kLoopSmemBra>"))
         if info["ops"] <= MINB_SMALL_OPS:
             # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads
-            out.append(("lane_t512", f"launch_class<Cls{cid}, 1, 1, 512>"))
-            out.append(("lane_t768", f"launch_class<Cls{cid}, 1, 1, 768>"))
-        if UNROLL2 and info["ops"] <= UNROLL2_MAX_OPS:
-            for m in mins:
-                out.append((f"lane_u2m{m}", f"launch_class<Cls{cid}, {m}, 2>"))
-            out.append(("lane_u2t512", f"launch_class<Cls{cid}, 1, 2, 512>"))
+            out.append(("lane_t512", f"launch_class<Cls{cid}, 1, kLoopPrefetch, 512>"))
+            out.append(("lane_t768", f"launch_class<Cls{cid}, 1, kLoopPrefetch, 768>"))
+            out.append(("lane_pp512", f"launch_class<Cls{cid}, 1, kLoopPingPong, 512>"))
+            out.append(("lane_pl512", f"launch_class<Cls{cid}, 1, kLoopPlain, 512>"))
+            out.append(("lane_pl768", f"launch_class<Cls{cid}, 1, kLoopPlain, 768>"))
+            out.append(("lane_sb512", f"launch_class<Cls{cid}, 1, kLoopSmemBra, 512>"))
+        if info["ops"] <= UNROLL2_MAX_OPS:
+            out.append(("lane_u2t512", f"launch_class<Cls{cid}, 1, kLoopTwoKet, 512>"))
+            out.append(("lane_pl1024", f"launch_class<Cls{cid}, 1, kLoopPlain, 1024>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
+    assert len(out) <= 12, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 
 
@@ -391,8 +327,8 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         la, lb, lc, ld = info["cls"]
         cid = class_id(info["cls"])
         vs = info["variants"]
-        fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (8 - len(vs))
-        names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (8 - len(vs))
+        fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (12 - len(vs))
+        names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (12 - len(vs))
         reg.append(f"  {{{la}, {lb}, {lc}, {ld}, {info['M']}, {info['ops']}, {info['prim_terms']}, "
                    f"{info['base']}, {info['contract']}, {info['hrr_terms']}, {len(vs)}, {{{fns}}}, "
                    f"{{{names}}}, {info['default']}}},")

@@ -62,6 +62,15 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
 // (for 40 <= T < 80 shifted by e^-40; 0 above 80, < 2e-35), so both branches
 // share one short polynomial. Rows are kBoysCols = 10 doubles, 16-byte
 // aligned, read as double2.
+// Non-immediate FP64 constants of boys_eval live in the constant bank so
+// DFMA/DMUL read them as c[][] operands instead of re-materialising them
+// with register moves inside the primitive loop.
+static __constant__ double kBoysK[10] = {
+    1.66666666666666667e-01, 4.16666666666666667e-02, 8.33333333333333333e-03,
+    1.38888888888888889e-03, 1.98412698412698413e-04, 2.48015873015873016e-05,
+    6755399441055744.0 /* 1.5 * 2^52 */, 4.24835425529158899e-18 /* e^-40 */,
+    0.88622692545275801365 /* sqrt(pi)/2 */, 0.0};
+
 template <int M>
 __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ tab, double* F) {
   const bool small = T < kBoysTmax;
@@ -69,48 +78,144 @@ __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ t
   const double* row;
   double md;
   {
-    const double Tt = small ? T : (T < 2.0 * kBoysTmax ? T - kBoysTmax : 0.0);
-    const int i = __double2int_rn(Tt * 16.0);
-    md = fma(static_cast<double>(i), 0.0625, -Tt);  // -(Tt - T_i)
+    // T_i = round(16 Tt)/16 by the 1.5*2^52 shift (no F2I/I2F round trip):
+    // the low word of the shifted value is the row index
+    double Tt;
+    if constexpr (M == 0)
+      Tt = small ? T : 0.0;  // no e^-T needed above the table
+    else
+      Tt = small ? T : (T < 2.0 * kBoysTmax ? T - kBoysTmax : 0.0);
+    const double sh = fma(Tt, 16.0, kBoysK[6]);
+    const int i = __double2loint(sh);
+    md = fma(sh - kBoysK[6], 0.0625, -Tt);  // -(Tt - T_i)
     row = tab + i * kBoysCols;
     if (M > 0) {
-      // exp(-d) = sum_k (-d)^k / k!, k <= 8 (|d| <= 1/32)
-      e = 2.48015873015873016e-05;
-      e = fma(e, md, 1.98412698412698413e-04);
-      e = fma(e, md, 1.38888888888888889e-03);
-      e = fma(e, md, 8.33333333333333333e-03);
-      e = fma(e, md, 4.16666666666666667e-02);
-      e = fma(e, md, 1.66666666666666667e-01);
-      e = fma(e, md, 0.5);
-      e = fma(e, md, 1.0);
-      e = fma(e, md, 1.0);
-      const double scale = small ? 1.0 : (T < 2.0 * kBoysTmax ? 4.24835425529158899e-18 : 0.0);  // e^-40
+      // exp(-d) = sum_k (-d)^k / k!, k <= 8 (|d| <= 1/32), Estrin form
+      // (dependency depth 4 instead of 8: the loop is latency-bound)
+      const double m2 = md * md, m4 = m2 * m2;
+      const double e01 = md + 1.0, e23 = fma(md, kBoysK[0], 0.5);
+      const double e45 = fma(md, kBoysK[2], kBoysK[1]);
+      const double e67 = fma(md, kBoysK[4], kBoysK[3]);
+      const double e0123 = fma(m2, e23, e01), e4567 = fma(m2, e67, e45);
+      e = fma(m4, fma(m4, kBoysK[5], e4567), e0123);
+      const double scale = small ? 1.0 : (T < 2.0 * kBoysTmax ? kBoysK[7] : 0.0);  // e^-40
       e *= row[8] * scale;
     }
   }
   if (small) {
     const double2* r = reinterpret_cast<const double2*>(row);
     const double2 c01 = r[0], c23 = r[1], c45 = r[2], c67 = r[3];
-    double f = fma(c67.y, md, c67.x);
-    f = fma(f, md, c45.y);
-    f = fma(f, md, c45.x);
-    f = fma(f, md, c23.y);
-    f = fma(f, md, c23.x);
-    f = fma(f, md, c01.y);
-    f = fma(f, md, c01.x);
-    F[M] = f;
+    // Estrin: depth 3 FMAs after the loads instead of a 7-deep Horner chain
+    const double m2 = md * md;
+    const double p01 = fma(c01.y, md, c01.x), p23 = fma(c23.y, md, c23.x);
+    const double p45 = fma(c45.y, md, c45.x), p67 = fma(c67.y, md, c67.x);
+    const double q0 = fma(p23, m2, p01), q1 = fma(p67, m2, p45);
+    F[M] = fma(q1, m2 * m2, q0);
     const double T2 = 2.0 * T;
 #pragma unroll
     for (int m = M; m > 0; --m) F[m - 1] = fma(T2, F[m], e) * (1.0 / (2 * m - 1));
   } else {
     const double rt = rsqrt_pos(T);
-    F[0] = 0.88622692545275801365 * rt;  // sqrt(pi)/2
+    F[0] = kBoysK[8] * rt;  // sqrt(pi)/2
     if (M > 0) {
       const double h = 0.5 * rt * rt;  // 1/(2T)
 #pragma unroll
       for (int m = 0; m < M; ++m) F[m + 1] = fma(static_cast<double>(2 * m + 1), F[m], -e) * h;
     }
   }
+}
+
+// Primitive loop nests over the class's prim()/finish() (compiler/
+// emit_cuda.py). Every style evaluates the same terms in the same order per
+// accumulator; they differ in how bra records are staged in registers:
+//  kLoopPlain     load each record where it is used (compiler schedules);
+//  kLoopPrefetch  next bra record loaded one step ahead (register rotation);
+//  kLoopTwoKet    two ket primitives per step share one bra record; two
+//                 accumulator sets, folded at the end;
+//  kLoopPingPong  bra loop unrolled by two with two record buffers, each
+//                 reloaded right after use (no register rotation copies).
+//  kLoopSmemBra   plain loop; when all lanes of the warp share the bra, its
+//                 primitive records are staged once in shared memory (per
+//                 warp, reused while consecutive items keep the bra).
+constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopTwoKet = 2, kLoopPingPong = 3, kLoopSmemBra = 4;
+constexpr int kSmemBraMax = 81;  // records per warp buffer (cc-pVDZ s9 x s9)
+
+// Generic-address record load (the pointer may be shared or global).
+template <bool WithPA = true>
+__device__ __forceinline__ PrimRec load_prim_gen(const PrimRec* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = q[0], b = q[1], c = q[2];
+  PrimRec r;
+  r.p = a.x; r.U = a.y; r.Px = b.x; r.Py = b.y; r.Pz = c.x; r.i2p = c.y;
+  if (WithPA) {
+    const double2 d = q[3], e = q[4];
+    r.PAx = d.x; r.PAy = d.y; r.PAz = e.x;
+  } else {
+    r.PAx = r.PAy = r.PAz = 0.0;
+  }
+  r.pad = 0.0;
+  return r;
+}
+
+template <class C, int STYLE>
+__device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int kb,
+                                          const PrimRec* __restrict__ ket, int kk, double ABx, double ABy,
+                                          double ABz, double CDx, double CDy, double CDz,
+                                          const double* __restrict__ btab, double (&out)[C::NV]) {
+  typename C::Acc a;
+  C::zero(a);
+  if constexpr (STYLE == kLoopPlain) {
+    for (int j = 0; j < kk; ++j) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      for (int i = 0; i < kb; ++i) C::prim(load_prim<C::BPA>(bra + i), kp, btab, a);
+    }
+  } else if constexpr (STYLE == kLoopSmemBra) {
+    for (int j = 0; j < kk; ++j) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
+    }
+  } else if constexpr (STYLE == kLoopPrefetch) {
+    for (int j = 0; j < kk; ++j) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      PrimRec bn = load_prim<C::BPA>(bra);
+      for (int i = 0; i < kb; ++i) {
+        const PrimRec bq = bn;
+        bn = load_prim<C::BPA>(bra + (i + 1 < kb ? i + 1 : i));
+        C::prim(bq, kp, btab, a);
+      }
+    }
+  } else if constexpr (STYLE == kLoopTwoKet) {
+    typename C::Acc b;
+    C::zero(b);
+    int j = 0;
+    for (; j + 1 < kk; j += 2) {
+      const PrimRec k0 = load_prim<C::KPA>(ket + j);
+      const PrimRec k1 = load_prim<C::KPA>(ket + j + 1);
+      for (int i = 0; i < kb; ++i) {
+        const PrimRec bq = load_prim<C::BPA>(bra + i);
+        C::prim(bq, k0, btab, a);
+        C::prim(bq, k1, btab, b);
+      }
+    }
+    if (j < kk) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      for (int i = 0; i < kb; ++i) C::prim(load_prim<C::BPA>(bra + i), kp, btab, a);
+    }
+    C::fold(a, b);
+  } else {
+    for (int j = 0; j < kk; ++j) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      PrimRec b0 = load_prim<C::BPA>(bra);
+      PrimRec b1 = load_prim<C::BPA>(bra + (kb > 1 ? 1 : 0));
+      for (int i = 0; i < kb; i += 2) {
+        C::prim(b0, kp, btab, a);
+        b0 = load_prim<C::BPA>(bra + (i + 2 < kb ? i + 2 : kb - 1));
+        if (i + 1 < kb) C::prim(b1, kp, btab, a);
+        b1 = load_prim<C::BPA>(bra + (i + 3 < kb ? i + 3 : kb - 1));
+      }
+    }
+  }
+  C::finish(a, ABx, ABy, ABz, CDx, CDy, CDz, out);
 }
 
 // Component normalisation (molecule.hpp:207-213) for L <= 4, x-major order.
@@ -127,6 +232,25 @@ __device__ __forceinline__ double comp_scale(int L, int i) {
   if (L == 2) return s2[i];
   if (L == 3) return s3[i];
   return s4[i];
+}
+
+// Pair metadata re-read after the primitive loop (ints only: first basis
+// functions and shells). asm volatile keeps the load where it is written.
+__device__ __forceinline__ void ld_meta_late(const PairMeta* p, PairMeta& m) {
+  int a, b, c, d, e, f, g, h;
+  asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
+  asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(e), "=r"(f), "=r"(g), "=r"(h) : "l"(reinterpret_cast<const char*>(p) + 16));
+  m.prim_off = a; m.K = b; m.bfa = c; m.bfb = d; m.sha = e; m.shb = f; m.ref = g; m.pad = h;
+}
+
+// FP64 reduction into J/K. ERITILE_PROBE_NODIGEST (a measurement-only build,
+// never the product) keeps the digestion arithmetic but drops the atomics.
+__device__ __forceinline__ void red_add(double* p, double v) {
+#ifdef ERITILE_PROBE_NODIGEST
+  if (v == 1.2345e-300) atomicAdd(p, v);
+#else
+  atomicAdd(p, v);
+#endif
 }
 
 // Inclusive segmented sum over lanes with equal non-decreasing key; lanes
@@ -150,9 +274,7 @@ __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* bo
 
 constexpr int kJkThreads = 256;
 
-// U = 1: C::eri (one primitive quartet per step); U = 2: C::eri2 (two ket
-// primitives per step sharing the bra record, two independent FMA chains).
-template <class C, int MINB, int U = 1, int NT = kJkThreads>
+template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
 __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
                                                        const PairMeta* __restrict__ pm,
@@ -164,6 +286,10 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
   load_boys_slice(s_boys, boys_tab, C::M);
 
   const int lane = threadIdx.x & 31;
+  PrimRec* sbra = reinterpret_cast<PrimRec*>(s_boys + kBoysRows * kBoysCols) + (threadIdx.x >> 5) * kSmemBraMax;
+  int staged = -1;  // bra pair whose records sit in sbra (warp-uniform)
+  (void)sbra;
+  (void)staged;
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   for (long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
        w < nitems; w += warps) {
@@ -179,15 +305,42 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
       ++c;
     }
     const int y = it.yfirst + q;
-    const PairMeta bm = pm[x];
-    const PairMeta km = pm[y];
     double v[C::NV];
-    if constexpr (U == 2)
-      C::eri2(prims + bm.prim_off, bm.K, prims + km.prim_off, active ? km.K : 0, bm.ABx, bm.ABy, bm.ABz,
-              km.ABx, km.ABy, km.ABz, s_boys, v);
-    else
-      C::eri(prims + bm.prim_off, bm.K, prims + km.prim_off, active ? km.K : 0, bm.ABx, bm.ABy, bm.ABz,
-             km.ABx, km.ABy, km.ABz, s_boys, v);
+    {
+      // only what the integral loop needs is loaded here; the digestion
+      // fields are re-read after it (asm volatile: not hoisted across the
+      // loop), so they occupy no registers during the primitive loop
+      const int4 bh = __ldg(reinterpret_cast<const int4*>(pm + x));
+      const int4 kh = __ldg(reinterpret_cast<const int4*>(pm + y));
+      double ABx = 0.0, ABy = 0.0, ABz = 0.0, CDx = 0.0, CDy = 0.0, CDz = 0.0;
+      if constexpr (C::LB > 0) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(&pm[x].ABx));
+        ABx = a.x; ABy = a.y; ABz = __ldg(&pm[x].ABz);
+      }
+      if constexpr (C::LD > 0) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(&pm[y].ABx));
+        CDx = a.x; CDy = a.y; CDz = __ldg(&pm[y].ABz);
+      }
+      const PrimRec* brap = prims + bh.x;
+      if constexpr (STYLE == kLoopSmemBra) {
+        const int x0 = __shfl_sync(0xffffffffu, x, 0);
+        if (__all_sync(0xffffffffu, x == x0) && bh.y <= kSmemBraMax) {
+          if (x0 != staged) {
+            __syncwarp();
+            const double2* src = reinterpret_cast<const double2*>(prims + bh.x);
+            double2* dst = reinterpret_cast<double2*>(sbra);
+            for (int t = lane; t < bh.y * 5; t += 32) dst[t] = __ldg(src + t);
+            __syncwarp();
+            staged = x0;
+          }
+          brap = sbra;
+        }
+      }
+      eri_drive<C, STYLE>(brap, bh.y, prims + kh.x, active ? kh.y : 0, ABx, ABy, ABz, CDx, CDy, CDz, s_boys, v);
+    }
+    PairMeta bm, km;
+    ld_meta_late(pm + x, bm);
+    ld_meta_late(pm + y, km);
     const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (x != y ? 2.0 : 1.0);
     const double wj = active ? 0.5 * deg : 0.0;
     const double wk = active ? 0.25 * deg : 0.0;
@@ -213,7 +366,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
           for (int d = 0; d < C::ND; ++d)
             s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dcd + c2 * n + d), s);
         s = seg_sum(s * wj, xkey, lane);
-        if (tail) atomicAdd(J + (bm.bfa + a) * n + bm.bfb + b, s);
+        if (tail) red_add(J + (bm.bfa + a) * n + bm.bfb + b, s);
       }
     if (active) {
 #pragma unroll
@@ -226,7 +379,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int b = 0; b < C::NB; ++b)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dab + a * n + b), s);
-          atomicAdd(J + (km.bfa + c2) * n + km.bfb + d, s * wj);
+          red_add(J + (km.bfa + c2) * n + km.bfb + d, s * wj);
         }
       // K_ac += sum_bd v D_bd ; K_bd += sum_ac v D_ac
 #pragma unroll
@@ -239,7 +392,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbd + b * n + d), s);
-          atomicAdd(K + (bm.bfa + a) * n + km.bfa + c2, s * wk);
+          red_add(K + (bm.bfa + a) * n + km.bfa + c2, s * wk);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
@@ -251,7 +404,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int c2 = 0; c2 < C::NC; ++c2)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dac + a * n + c2), s);
-          atomicAdd(K + (bm.bfb + b) * n + km.bfb + d, s * wk);
+          red_add(K + (bm.bfb + b) * n + km.bfb + d, s * wk);
         }
       // K_ad += sum_bc v D_bc ; K_bc += sum_ad v D_ad
 #pragma unroll
@@ -264,7 +417,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int c2 = 0; c2 < C::NC; ++c2)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbc + b * n + c2), s);
-          atomicAdd(K + (bm.bfa + a) * n + km.bfb + d, s * wk);
+          red_add(K + (bm.bfa + a) * n + km.bfb + d, s * wk);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
@@ -276,7 +429,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dad + a * n + d), s);
-          atomicAdd(K + (bm.bfb + b) * n + km.bfa + c2, s * wk);
+          red_add(K + (bm.bfb + b) * n + km.bfa + c2, s * wk);
         }
     }
   }
@@ -337,16 +490,17 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 // NT: threads per CTA. One Boys slice is staged per CTA, so 512/768-thread
 // CTAs at MINB = 1 keep 16/24 warps per SM with a single 51 KB table and
 // leave the rest of the 256 KB L1/shared array to L1 (primitive records).
-template <class C, int MINB, int U = 1, int NT = kJkThreads>
+template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
 void launch_class(const LaunchArgs& a) {
-  const size_t smem = sizeof(double) * kBoysRows * kBoysCols;
+  const size_t smem = sizeof(double) * kBoysRows * kBoysCols +
+                      (STYLE == kLoopSmemBra && a.mode == 0 ? sizeof(PrimRec) * kSmemBraMax * (NT / 32) : 0);
   if (a.mode == 0) {
     if (a.nitems <= 0) return;
     static int blocks_per_sm = 0;
     static int sms = 0;
     if (!blocks_per_sm) {
-      cudaFuncSetAttribute(jk_kernel<C, MINB, U, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C, MINB, U, NT>, NT, smem);
+      cudaFuncSetAttribute(jk_kernel<C, MINB, STYLE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C, MINB, STYLE, NT>, NT, smem);
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -355,7 +509,7 @@ void launch_class(const LaunchArgs& a) {
     const long long want = (a.nitems + (NT / 32) - 1) / (NT / 32);
     const long long cap = static_cast<long long>(blocks_per_sm) * sms;
     const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
-    jk_kernel<C, MINB, U, NT><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
+    jk_kernel<C, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
                                                        a.K, a.N, a.boys_tab);
   } else if (a.mode == 2) {
     if (a.nq <= 0) return;

@@ -304,13 +304,13 @@ class Engine:
         """{class: {variant name: median ms}} of the last tune."""
         n = self._lib.eritile_gpu_tune_times(self._h, 0, None, None)
         ci = np.zeros(max(n, 1), np.int32)
-        ms = np.zeros(8 * max(n, 1))
+        ms = np.zeros(12 * max(n, 1))
         self._lib.eritile_gpu_tune_times(self._h, n, ci.ctypes.data, ms.ctypes.data)
         tab = class_table()
         out = {}
         for w in range(n):
             names = variant_names(int(ci[w]))
-            out["".join(map(str, tab[ci[w]][:4]))] = {nm: round(float(ms[8 * w + v]), 4) for v, nm in enumerate(names)}
+            out["".join(map(str, tab[ci[w]][:4]))] = {nm: round(float(ms[12 * w + v]), 4) for v, nm in enumerate(names)}
         return out
 
     def variants(self) -> dict:
