@@ -28,7 +28,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-METRIC = "Fock-build ERI quartets/s ((H2O)_80 cc-pVDZ, N=2000, Schwarz tau=1e-10)"
+METRIC = "Fock-build ERI quartets/s ((H2O)_{waters} {basis}, Schwarz tau={tau:g})"
 UNIT = "quartets/s"
 
 
@@ -244,6 +244,9 @@ def run_ours(args, rank, nranks, local_rank):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
+    prof_range = os.environ.get("ERITILE_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
+    if prof_range:
+        torch.cuda.profiler.start()
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
             flush.fill_(float(k))
@@ -251,6 +254,8 @@ def run_ours(args, rank, nranks, local_rank):
             step()
             ev[k][1].record(stream)
         torch.cuda.synchronize()
+    if prof_range:
+        torch.cuda.profiler.stop()
     if dist is not None:
         dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
@@ -288,6 +293,7 @@ def run_ours(args, rank, nranks, local_rank):
         del eng
         e0 = Engine(local_rank).load_molecule(xyz, basis).build_pairs(0.0)
         e0.set_screening(args.tau)
+        e0.tune(Dh, reps=1)
         s0 = e0.stats()
         e0.build_jk_partial_device(D.data_ptr(), JK.data_ptr(), sp)
         ev0 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
@@ -333,7 +339,7 @@ def run_ours(args, rank, nranks, local_rank):
                 "peak_source": peak_src,
                 "flops_model": "SURVEY.md 8d: F_c = Nprim(42+3m+2(P+B+X)) + Nq(2H+12n), executed plan"}
     out = {
-        "metric": METRIC, "value": q_tot / (ms * 1e-3), "unit": UNIT, "n_gpus": nranks, "steps": args.steps,
+        "metric": METRIC.format(waters=args.waters, basis=args.basis, tau=args.tau), "value": q_tot / (ms * 1e-3), "unit": UNIT, "n_gpus": nranks, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic water-cluster geometry, seeded density)",
         "config": dict(config(args, nranks), n_basis=N),
@@ -351,7 +357,9 @@ def run_ours(args, rank, nranks, local_rank):
         "tune_ms": tune_table,
         "classes": [{"cls": "".join(map(str, r["cls"])), "ms": round(r["ms"], 4),
                      "variant": chosen.get(tuple(r["cls"])),
-                     "tflops": r["flops"] / max(r["ms"], 1e-9) / 1e9, "quartets": r["quartets"]}
+                     "tflops": r["flops"] / max(r["ms"], 1e-9) / 1e9, "quartets": r["quartets"],
+                     "prim_quartets": r["prim_quartets"],
+                     "ns_per_prim_quartet_sm": r["ms"] * 1e6 * 148 / max(r["prim_quartets"], 1)}
                     for r in sorted(prof, key=lambda r: -r["ms"])],
     }
     if not args.no_cpu and nranks == 1:
@@ -369,7 +377,7 @@ def run_reference(args, rank):
     if rank != 0:
         return None
     cb = cpu_sample(args, steps=args.steps, warmup=args.warmup, target_s=args.cpu_seconds, reference_arm=True)
-    return {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    return {"metric": METRIC.format(waters=args.waters, basis=args.basis, tau=args.tau), "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic water-cluster geometry, seeded density)",
             "config": dict(config(args, 1), n_basis=cb["n_basis"]), "impl": "reference",

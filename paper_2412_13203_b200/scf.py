@@ -100,10 +100,96 @@ def rhf(build_jk: Callable[[np.ndarray], tuple], S: np.ndarray, H: np.ndarray, e
     return res
 
 
-def run_rhf(xyz_text: str, basis_text: str, tau: float = 1e-12, device: int = 0, **kw) -> ScfResult:
-    """Full driver on one GPU: load, pairs, Schwarz, screening, SCF."""
+def rhf_device(engine, S: np.ndarray, H: np.ndarray, e_nuc: float, nocc: int, conv: float = 1e-6,
+               max_iter: int = 99, diis: bool = True, e_conv: float = 1e-10) -> ScfResult:
+    """Device-resident Roothaan/DIIS loop: D, J, K, F and
+    the DIIS history stay in HBM; the Fock build is ``build_jk_device`` on
+    the current torch stream, the orthogonalised eigenproblem is
+    ``torch.linalg.eigh`` (cuSOLVER syevd) and D = C_occ C_occ^T a DGEMM.
+    Only the energy and the convergence scalars come back to the host."""
+    import torch
+    stream = torch.cuda.Stream()  # one explicit stream for torch ops and the Fock build
+    with torch.cuda.stream(stream):
+        return _rhf_device(engine, S, H, e_nuc, nocc, conv, max_iter, diis, e_conv, stream.cuda_stream)
+
+
+def _rhf_device(engine, S, H, e_nuc, nocc, conv, max_iter, diis, e_conv, st) -> ScfResult:
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = lambda a: torch.as_tensor(a, dtype=torch.float64, device=dev).contiguous()
+    Sd, Hd = t(S), t(H)
+    X = t(orthogonalizer(S))
+    N = Hd.shape[0]
+    J = torch.empty((N, N), dtype=torch.float64, device=dev)
+    K = torch.empty_like(J)
+
+    def fock_build(D):
+        engine.build_jk_device(D.data_ptr(), J.data_ptr(), K.data_ptr(), st)
+        return J, K
+
+    def density(F):
+        _, Cp = torch.linalg.eigh(X.T @ F @ X)
+        C = X @ Cp[:, :nocc]
+        return C @ C.T
+
+    D = density(Hd).contiguous()
+    res = ScfResult(energy=0.0, iterations=0, converged=False)
+    focks, errs = [], []
+    E_old = None
+    for it in range(1, max_iter + 1):
+        J_, K_ = fock_build(D)
+        res.fock_builds += 1
+        F = Hd + 2.0 * J_ - K_
+        E = float(torch.sum(D * (Hd + F))) + e_nuc
+        if not np.isfinite(E):
+            raise FloatingPointError("SCF energy is not finite")
+        res.energies.append(E)
+        Fs = F
+        if diis:
+            focks.append(F.clone())
+            errs.append(X.T @ (F @ D @ Sd - Sd @ D @ F) @ X)
+            if len(focks) > 6:
+                focks.pop(0)
+                errs.pop(0)
+            n = len(focks)
+            if n >= 2:
+                E_ = torch.stack(errs).reshape(n, -1)
+                B = -torch.ones((n + 1, n + 1), dtype=torch.float64, device=dev)
+                B[n, n] = 0.0
+                B[:n, :n] = E_ @ E_.T
+                rhs = torch.zeros(n + 1, dtype=torch.float64, device=dev)
+                rhs[n] = -1.0
+                try:
+                    c = torch.linalg.solve(B, rhs)[:n]
+                    Fs = torch.einsum("i,ijk->jk", c, torch.stack(focks))
+                except RuntimeError:
+                    Fs = F
+        Dn = density(Fs).contiguous()
+        dD = float(torch.max(torch.abs(Dn - D)))
+        D = Dn
+        res.iterations = it
+        if dD < conv and (E_old is not None and abs(E - E_old) < e_conv):
+            res.converged = True
+            break
+        E_old = E
+    J_, K_ = fock_build(D)
+    res.fock_builds += 1
+    F = Hd + 2.0 * J_ - K_
+    res.energy = float(torch.sum(D * (Hd + F))) + e_nuc
+    res.density = D.cpu().numpy()
+    return res
+
+
+def run_rhf(xyz_text: str, basis_text: str, tau: float = 1e-12, device: int = 0, kappa_screen: float = 0.0,
+            device_resident: bool = False, **kw) -> ScfResult:
+    """Full driver on one GPU: load, pairs, Schwarz, screening, SCF. With
+    ``device_resident`` the post-Fock step runs on the GPU too (rhf_device)."""
     from .eritile import Engine
-    e = Engine(device).load_molecule(xyz_text, basis_text).build_pairs(0.0)
+    e = Engine(device).load_molecule(xyz_text, basis_text).build_pairs(kappa_screen)
     e.set_screening(tau)
     S, T, V = e.one_electron()
+    if device_resident:
+        import torch
+        torch.cuda.set_device(device)
+        return rhf_device(e, S, T + V, e.nuclear_repulsion(), e.nelectrons // 2, **kw)
     return rhf(e.build_jk, S, T + V, e.nuclear_repulsion(), e.nelectrons // 2, **kw)

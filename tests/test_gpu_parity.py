@@ -160,7 +160,7 @@ def _force_variant(e, k):
         e.set_variant(i, min(k, len(names) - 1))
 
 
-@pytest.mark.parametrize("k", list(range(8)))
+@pytest.mark.parametrize("k", list(range(12)))
 def test_every_kernel_variant_eri_and_jk(gpu, k):
     """Every kernel variant (lane_m2 / lane_m3 / coop) of every class gives the
     oracle's integrals and J/K (benzene 6-31G* covers all L<=2 classes that

@@ -27,3 +27,14 @@ def test_scf_energy_vs_oracle(gpu, mol, basis, tau):
     assert abs(g.energy - o.energy) < 1e-8, (g.energy, o.energy)
     if (mol, basis) == ("water", "sto-3g"):
         assert abs(g.energy - (-74.9630231287)) < 1e-8
+
+
+@pytest.mark.parametrize("mol,basis,tau", [("water", "cc-pvdz", 1e-12), ("w4", "cc-pvdz", 1e-10)])
+def test_device_resident_scf_matches_host_scf(gpu, mol, basis, tau):
+    """the post-Fock step on the GPU (cuSOLVER eigh, DGEMM
+    density, device DIIS) reaches the same energy as the host driver."""
+    from paper_2412_13203_b200.scf import run_rhf
+    h = run_rhf(geom(mol), BASIS[basis], tau=tau, conv=1e-9, e_conv=1e-12)
+    d = run_rhf(geom(mol), BASIS[basis], tau=tau, conv=1e-9, e_conv=1e-12, device_resident=True)
+    assert h.converged and d.converged
+    assert abs(h.energy - d.energy) < 1e-8, (h.energy, d.energy)
