@@ -140,6 +140,13 @@ int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps);
  * each variant (kMaxVariants = 12 per launch, 0 = no such variant). */
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms);
 int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var);
+/* Shared-primitive units (generally contracted sibling shells evaluated once
+ * per primitive quartet, csrc/jk_family.cuh): on by default; classes with
+ * "fam_" variants then run only those. Takes effect at the next
+ * set_screening. Results and quartet lists are unchanged. */
+int eritile_gpu_set_families(eritile_gpu* ctx, int on);
+/* Active variant index range [lo, hi) of a class in this context. */
+int eritile_gpu_variant_range(const eritile_gpu* ctx, int cls_index, int* lo, int* hi);
 int eritile_gpu_get_variant(const eritile_gpu* ctx, int cls_index);
 int eritile_gpu_class_nvariants(int cls_index);
 const char* eritile_gpu_variant_name(int cls_index, int var);

@@ -175,6 +175,33 @@ def emit_class(cls) -> Tuple[str, Dict]:
     for ln in body:
         w("    " + ln)
     w("  }")
+    # family form (csrc/jk_family.cuh): U-free prefactor, two bra-member
+    # weights; the ket-member weights are applied per ket primitive (axpy)
+    w("  __device__ __forceinline__ static void prim_w(const PrimRec& bp, const PrimRec& kp,")
+    w("                                                const double* __restrict__ btab, double w0, double w1,")
+    w("                                                Acc& s0, Acc& s1) {")
+    bnd_lines = {f"a.{bnd_name[n]} += {lower_name[n]};": n for n in plan.boundary}
+    for ln in body:
+        if ln == "const double pref = bp.U * kp.U * rs;":
+            w("    const double pref = rs;")
+        elif ln in bnd_lines:
+            n = bnd_lines[ln]
+            w(f"    s0.{bnd_name[n]} = fma(w0, {lower_name[n]}, s0.{bnd_name[n]}); "
+              f"s1.{bnd_name[n]} = fma(w1, {lower_name[n]}, s1.{bnd_name[n]});")
+        else:
+            w("    " + ln)
+    w("  }")
+    w("  __device__ __forceinline__ static void prim_w1(const PrimRec& bp, const PrimRec& kp,")
+    w("                                                 const double* __restrict__ btab, double w0, Acc& s0) {")
+    for ln in body:
+        if ln == "const double pref = bp.U * kp.U * rs;":
+            w("    const double pref = rs * w0;")
+        else:
+            w("    " + ln.replace("a.t", "s0.t"))
+    w("  }")
+    w("  __device__ __forceinline__ static void axpy(Acc& a, double w, const Acc& s) {")
+    w("    " + " ".join(f"a.{bnd_name[n]} = fma(w, s.{bnd_name[n]}, a.{bnd_name[n]});" for n in plan.boundary))
+    w("  }")
     w("  __device__ __forceinline__ static void finish(const Acc& a, double ABx, double ABy, double ABz,")
     w("                                                double CDx, double CDy, double CDz, double (&out)[NV]) {")
     w("    (void)ABx; (void)ABy; (void)ABz; (void)CDx; (void)CDy; (void)CDz;")
@@ -225,7 +252,8 @@ LANE_MAX_OPS = int(os.environ.get("ERITILE_LANE_MAX_OPS", "4000"))
 COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2, 3)
-COOP_SMEM_BUDGET = 110 * 1024  # keep >= 2 CTAs/SM when the Boys slice is staged
+COOP_SMEM_BUDGET = 110 * 1024
+FAM_MAX_BOUNDARY = int(os.environ.get("ERITILE_FAM_MAX_BOUNDARY", "9"))  # keep >= 2 CTAs/SM when the Boys slice is staged
 
 
 def variants(info) -> List[Tuple[str, str]]:
@@ -252,12 +280,19 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("lane_pl1024", f"launch_class<Cls{cid}, 1, kLoopPlain, 1024>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
-    assert len(out) <= 12, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
+    if info["boundary"] <= FAM_MAX_BOUNDARY:
+        # shared-primitive unit kernels (csrc/jk_family.cuh); kept last: the
+        # engine uses these (and only these) when families are enabled
+        out.append(("fam_pl512", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512>"))
+        out.append(("fam_pl768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 768>"))
+        out.append(("fam_pf512", f"launch_fam<Cls{cid}, 1, kLoopPrefetch, 512>"))
+        out.append(("fam_m2", f"launch_fam<Cls{cid}, 2, kLoopPlain, 256>"))
+    assert len(out) <= 16, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 
 
 def default_variant(info, vs) -> int:
-    names = [v[0] for v in vs]
+    names = [v[0] for v in vs if not v[0].startswith("fam_")]
     if "coop" in names and (info["ops"] >= 2000 or len(names) == 1):
         return names.index("coop")
     return 0
@@ -279,7 +314,7 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         lane = any(n.startswith("lane") for n, _ in vs)
         coop = any(n == "coop" for n, _ in vs)
         src = ["// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
-               '#include "../jk_coop.cuh"', "namespace eritile_b200 {"]
+               '#include "../jk_coop.cuh"', '#include "../jk_family.cuh"', "namespace eritile_b200 {"]
         if lane:
             src.append(body)
         else:  # sizes only; the straight-line body is not emitted
@@ -310,7 +345,7 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
             src.append(f"  launch_coop<CoopCls{cid}>(t, a);")
             src.append("}")
         for name, expr in vs:
-            if name.startswith("lane"):
+            if name != "coop":
                 src.append(f"void launch_{name}_cls{cid}(const LaunchArgs& a) {{ {expr}(a); }}")
         src += ["}  // namespace eritile_b200", ""]
         _write_if_changed(outdir / f"cls_{cid}.cu", "\n".join(src))
@@ -327,11 +362,13 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         la, lb, lc, ld = info["cls"]
         cid = class_id(info["cls"])
         vs = info["variants"]
-        fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (12 - len(vs))
-        names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (12 - len(vs))
+        fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (16 - len(vs))
+        names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (16 - len(vs))
+        nfam = sum(1 for n, _ in vs if n.startswith("fam_"))
+        fam_def = len(vs) - nfam if nfam else -1
         reg.append(f"  {{{la}, {lb}, {lc}, {ld}, {info['M']}, {info['ops']}, {info['prim_terms']}, "
                    f"{info['base']}, {info['contract']}, {info['hrr_terms']}, {len(vs)}, {{{fns}}}, "
-                   f"{{{names}}}, {info['default']}}},")
+                   f"{{{names}}}, {info['default']}, {nfam}, {fam_def}}},")
     reg.append("};")
     reg.append(f"const int kNumClasses = {len(infos)};")
     reg.append(f"const int kMaxL = {lmax};")

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <stdexcept>
@@ -27,6 +28,7 @@
 #include "../../../include/eritile_gpu.h"
 #include "../jk_api.h"
 #include "../jk_kernels.cuh"
+#include "../jk_family.cuh"
 #include "molecule.h"
 #include "onee.h"
 
@@ -168,12 +170,15 @@ __global__ void k_boys(int m_max, const double* __restrict__ T, int n, const dou
 // ---------------------------------------------------------------- context
 struct Group {
   int la, lb, K;
-  int first, count;  // product pair ids
+  int first, count;  // product pair ids (units for unit groups)
+  int nm = 1;        // unit groups: members per unit
 };
 
 struct ClassWork {
   int cls;  // index into kClassTable
+  bool fam; // items index units (shared-primitive kernels)
   long long off, n;
+  long long seg[5] = {0, 0, 0, 0, 0};  // unit classes: (1,1)(1,2)(2,1)(2,2) member segments, relative
   long long quartets, prim_quartets;
   double flops = 0.0;    // model FLOPs of this class launch
   double last_ms = 0.0;  // device time of the last launch (profiling mode)
@@ -225,6 +230,43 @@ struct eritile_gpu {
   DevBuf<int> d_list;
   DevBuf<double> d_D, d_Ds, d_JK, d_J, d_K;
 
+  // shared-primitive units (csrc/jk_family.cuh)
+  bool families = true;
+  std::vector<int> sib;                 // sibling id per shell (centre, L, exponents)
+  std::vector<unsigned long long> fam_key_ref;  // per reference pair: prim-set signature
+  std::vector<int> fam_sib_ref;         // per reference pair: sib(A) * nshell + sib(B)
+  std::vector<UnitMeta> um;
+  std::vector<Group> ugroups;
+  std::vector<double> uQ;
+  std::vector<double2> uw;
+  DevBuf<UnitMeta> d_um;
+  DevBuf<double2> d_uw;
+  DevBuf<double> d_Qp;
+
+  // Classes with unit ("fam_") variants get both work lists (pair items and
+  // unit items); the chosen variant decides which one a build launches.
+  bool fam_active(int c) const { return families && kClassTable[c].nfam > 0; }
+  int var_lo(int) const { return 0; }
+  int var_hi(int c) const { return fam_active(c) ? kClassTable[c].nvar : kClassTable[c].nvar - kClassTable[c].nfam; }
+  bool uses_fam(int c) const { return fam_active(c) && variant(c) >= kClassTable[c].nvar - kClassTable[c].nfam; }
+  bool active(const ClassWork& cw) const { return cw.fam == uses_fam(cw.cls); }
+  std::vector<int> active_work() const {
+    std::vector<int> o;
+    for (size_t w = 0; w < work.size(); ++w)
+      if (active(work[w])) o.push_back(static_cast<int>(w));
+    return o;
+  }
+  // totals over the launches a build makes
+  void update_totals() {
+    quartets = prim_quartets = 0;
+    model_flops = 0.0;
+    for (int w : active_work()) {
+      quartets += work[w].quartets;
+      prim_quartets += work[w].prim_quartets;
+      model_flops += work[w].flops;
+    }
+  }
+
   // Workload Allocator state: kernel variant per class (kClassTable[c].var)
   std::vector<int> var_choice;
   std::vector<double> tune_ms;  // per class launch x kMaxVariants: median ms (tune)
@@ -241,7 +283,9 @@ struct eritile_gpu {
   }
 
   int variant(int c) const {
-    return var_choice.empty() ? kClassTable[c].def : var_choice[c];
+    const int v = var_choice.empty() ? -1 : var_choice[c];
+    if (v >= var_lo(c) && v < var_hi(c)) return v;
+    return kClassTable[c].def;
   }
 
   // Workload Allocator (Alg. 2): for every
@@ -253,7 +297,7 @@ struct eritile_gpu {
   void tune(const double* dDs, int reps) {
     if (var_choice.empty()) {
       var_choice.resize(kNumClasses);
-      for (int c = 0; c < kNumClasses; ++c) var_choice[c] = kClassTable[c].def;
+      for (int c = 0; c < kNumClasses; ++c) var_choice[c] = -1;
     }
     const size_t NN = static_cast<size_t>(nbf) * nbf;
     DevBuf<double> scratch;
@@ -261,16 +305,21 @@ struct eritile_gpu {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    tune_ms.assign(work.size() * kMaxVariants, 0.0);
-    for (size_t w = 0; w < work.size(); ++w) {
-      const ClassWork& cw = work[w];
-      const ClassEntry& ce = kClassTable[cw.cls];
+    tune_ms.assign(static_cast<size_t>(kNumClasses) * kMaxVariants, 0.0);
+    std::vector<int> pair_w(kNumClasses, -1), fam_w(kNumClasses, -1);
+    for (size_t w = 0; w < work.size(); ++w) (work[w].fam ? fam_w : pair_w)[work[w].cls] = static_cast<int>(w);
+    for (int c = 0; c < kNumClasses; ++c) {
+      if (pair_w[c] < 0 && fam_w[c] < 0) continue;
+      const ClassEntry& ce = kClassTable[c];
       double best = 1e300;
-      int bestv = var_choice[cw.cls];
-      for (int v = 0; v < ce.nvar; ++v) {
+      int bestv = variant(c);
+      for (int v = var_lo(c); v < var_hi(c); ++v) {
+        const bool famv = v >= ce.nvar - ce.nfam;
+        const int w = famv ? fam_w[c] : pair_w[c];
+        if (w < 0) continue;
         std::vector<double> t;
         for (int r = 0; r < reps + 1; ++r) {
-          LaunchArgs a = class_args(cw, dDs, scratch.p, stream);
+          LaunchArgs a = class_args(work[w], dDs, scratch.p, stream);
           CK(cudaEventRecord(e0, stream));
           ce.var[v](a);
           CK(cudaGetLastError());
@@ -280,14 +329,15 @@ struct eritile_gpu {
         }
         std::sort(t.begin(), t.end());
         const double med = t[t.size() / 2];
-        tune_ms[w * kMaxVariants + v] = med;
+        tune_ms[static_cast<size_t>(c) * kMaxVariants + v] = med;
         if (med < best) {
           best = med;
           bestv = v;
         }
       }
-      var_choice[cw.cls] = bestv;
+      var_choice[c] = bestv;
     }
+    update_totals();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
@@ -308,6 +358,13 @@ struct eritile_gpu {
     a.boys_tab = d_boys.p;
     a.stream = st;
     a.block = 128;
+    for (int k = 0; k < 5; ++k) a.seg[k] = cw.seg[k];
+    if (cw.fam) {
+      a.um = d_um.p;
+      a.uw = d_uw.p;
+      a.Qp = d_Qp.p;
+      a.tau = tau;
+    }
     return a;
   }
 
@@ -335,6 +392,18 @@ struct eritile_gpu {
       for (auto& c : comps) bf_scale.push_back(component_scale(c[0], c[1], c[2]));
     }
     nbf = bf_off.back();
+    // sibling shells: same centre, L and exponents (general contractions
+    // written in segmented form, e.g. cc-pVDZ O 1s/2s)
+    {
+      std::map<std::vector<double>, int> ids;
+      sib.assign(shells.size(), 0);
+      for (size_t i = 0; i < shells.size(); ++i) {
+        std::vector<double> k = {shells[i].c[0], shells[i].c[1], shells[i].c[2], static_cast<double>(shells[i].L)};
+        k.insert(k.end(), shells[i].exps.begin(), shells[i].exps.end());
+        auto it = ids.emplace(k, static_cast<int>(ids.size())).first;
+        sib[i] = it->second;
+      }
+    }
     have_mol = true;
     have_pairs = have_q = have_lists = false;
     if (!host_only) d_scale.upload(bf_scale);
@@ -347,6 +416,7 @@ struct eritile_gpu {
     struct Tmp {
       int i, j, li, lj;
       std::vector<PrimRec> pr;
+      unsigned long long sig = 1469598103934665603ull;  // FNV-1a of kept (k, l)
     };
     std::vector<Tmp> all;
     all.reserve(static_cast<size_t>(S) * (S + 1) / 2);
@@ -382,6 +452,7 @@ struct eritile_gpu {
             r.i2p = 0.5 / p;
             r.pad = 0.0;
             t.pr.push_back(r);
+            t.sig = (t.sig ^ static_cast<unsigned long long>(k * 4096 + l)) * 1099511628211ull;
           }
         if (kappa_screen > 0.0 && t.pr.empty()) continue;
         all.push_back(std::move(t));
@@ -398,11 +469,18 @@ struct eritile_gpu {
     const int np = static_cast<int>(all.size());
     ref_i.resize(np);
     ref_j.resize(np);
+    fam_key_ref.resize(np);
+    fam_sib_ref.resize(np);
     std::vector<int> ref_of_tmp(np);
     for (int r = 0; r < np; ++r) {
-      ref_i[r] = all[order[r]].i;
-      ref_j[r] = all[order[r]].j;
+      const Tmp& t = all[order[r]];
+      ref_i[r] = t.i;
+      ref_j[r] = t.j;
       ref_of_tmp[order[r]] = r;
+      const bool sw = t.lj > t.li;
+      const int A = sw ? t.j : t.i, B = sw ? t.i : t.j;
+      fam_key_ref[r] = t.sig ^ (static_cast<unsigned long long>(t.pr.size()) << 48);
+      fam_sib_ref[r] = sib[A] * static_cast<int>(shells.size()) + sib[B];
     }
     // product grouping: key (LA+LB, LA, LB, K), then reference index
     std::vector<int> pord(np);
@@ -524,27 +602,131 @@ struct eritile_gpu {
     if (!host_only) d_pm.upload(pm);
   }
 
+  // Units of <= kFamMax product pairs with identical primitive records up to
+  // U: same oriented sibling shells and the same kept primitive index set,
+  // taken in Q-descending order inside each product group. Unit groups are
+  // keyed (L_A+L_B, L_A, L_B, K, members) and sorted by unit Q = max member Q.
+  void build_units() {
+    um.clear();
+    ugroups.clear();
+    uQ.clear();
+    std::vector<UnitMeta> tmp;
+    std::vector<double> tq;
+    for (const Group& g : groups) {
+      std::map<std::pair<int, unsigned long long>, std::vector<int>> buckets;
+      std::vector<std::pair<int, unsigned long long>> order;
+      for (int x = g.first; x < g.first + g.count; ++x) {
+        const int r = pm[x].ref;
+        auto key = std::make_pair(fam_sib_ref[r], fam_key_ref[r]);
+        auto it = buckets.find(key);
+        if (it == buckets.end()) {
+          order.push_back(key);
+          it = buckets.emplace(key, std::vector<int>{}).first;
+        }
+        it->second.push_back(x);
+      }
+      std::vector<UnitMeta> units[kFamMax + 1];
+      std::vector<double> uq[kFamMax + 1];
+      for (const auto& key : order) {
+        const std::vector<int>& v = buckets[key];
+        for (size_t s0 = 0; s0 < v.size(); s0 += kFamMax) {
+          const int nm = static_cast<int>(std::min<size_t>(kFamMax, v.size() - s0));
+          UnitMeta u{};
+          u.prim_off = pm[v[s0]].prim_off;
+          u.K = pm[v[s0]].K;
+          u.nm = nm;
+          u.m0 = v[s0];
+          u.m1 = nm > 1 ? v[s0 + 1] : v[s0];
+          u.ABx = pm[v[s0]].ABx;
+          u.ABy = pm[v[s0]].ABy;
+          u.ABz = pm[v[s0]].ABz;
+          units[nm].push_back(u);
+          uq[nm].push_back(std::max(Q.empty() ? 0.0 : Q[u.m0], Q.empty() ? 0.0 : Q[u.m1]));
+        }
+      }
+      for (int nm = 1; nm <= kFamMax; ++nm) {
+        if (units[nm].empty()) continue;
+        std::vector<int> o(units[nm].size());
+        std::iota(o.begin(), o.end(), 0);
+        std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return uq[nm][a] > uq[nm][b]; });
+        Group ug{g.la, g.lb, g.K, static_cast<int>(um.size()), static_cast<int>(o.size()), nm};
+        for (int k : o) {
+          um.push_back(units[nm][k]);
+          uQ.push_back(uq[nm][k]);
+        }
+        ugroups.push_back(ug);
+      }
+    }
+    uw.assign(prims.size(), double2{0.0, 0.0});
+    for (const UnitMeta& u : um)
+      for (int i = 0; i < u.K; ++i) {
+        uw[u.prim_off + i].x = prims[pm[u.m0].prim_off + i].U;
+        uw[u.prim_off + i].y = u.nm > 1 ? prims[pm[u.m1].prim_off + i].U : 0.0;
+      }
+    if (!host_only) {
+      d_um.upload(um);
+      d_uw.upload(uw);
+      d_Qp.upload(Q.empty() ? std::vector<double>(pm.size(), 0.0) : Q);
+    }
+  }
+
+  // Member quartets of unit pair (u, v) that survive (Q_m Q_n >= tau) and
+  // are canonical (u == v: members m <= n only).
+  int unit_pair_quartets(int u, int v, double t) const {
+    const UnitMeta& a = um[u];
+    const UnitMeta& b = um[v];
+    int c = 0;
+    for (int m = 0; m < a.nm; ++m)
+      for (int n = 0; n < b.nm; ++n) {
+        if (u == v && m > n) continue;
+        const int x = m ? a.m1 : a.m0, y = n ? b.m1 : b.m0;
+        if (t <= 0.0 || Q[x] * Q[y] >= t) ++c;
+      }
+    return c;
+  }
+
   void set_screening(double t) {
     if (!have_pairs) throw StateError("set_screening before build_pairs");
     if (t > 0.0 && !have_q) schwarz();
     tau = t;
     if (t > 0.0) sort_groups_by_q();
-    // enumerate group pairs X >= Y, grouped by angular class
+    bool any_fam = false;
+    for (int c = 0; c < kNumClasses; ++c) any_fam = any_fam || fam_active(c);
+    if (any_fam) build_units();
+    // enumerate group pairs X >= Y (pair groups, or unit groups for classes
+    // served by the shared-primitive kernels), grouped by angular class
     struct GP {
       int X, Y, cls;
+      bool fam;
       long long cost;
+      int seg = 0;  // unit classes: (nm_x - 1) * 2 + (nm_y - 1)
     };
     std::vector<GP> gps;
     for (int X = 0; X < static_cast<int>(groups.size()); ++X)
       for (int Y = 0; Y <= X; ++Y) {
         const Group& gx = groups[X];
         const Group& gy = groups[Y];
-        GP gp{X, Y, class_index(gx.la, gx.lb, gy.la, gy.lb),
-              static_cast<long long>(gx.K) * gy.K};
-        gps.push_back(gp);
+        const int cls = class_index(gx.la, gx.lb, gy.la, gy.lb);
+        gps.push_back(GP{X, Y, cls, false, static_cast<long long>(gx.K) * gy.K});
       }
+    if (any_fam) {
+      // unit group order: (L_A+L_B, L_A, L_B, K) as the pair groups, so the
+      // bra/ket roles of a quartet (X >= Y) follow the pair path's rule
+      auto gkey = [](const Group& g) { return std::make_tuple(g.la + g.lb, g.la, g.lb, g.K); };
+      for (int X = 0; X < static_cast<int>(ugroups.size()); ++X)
+        for (int Y = 0; Y < static_cast<int>(ugroups.size()); ++Y) {
+          const Group& gx = ugroups[X];
+          const Group& gy = ugroups[Y];
+          if (gkey(gx) < gkey(gy) || (gkey(gx) == gkey(gy) && X < Y)) continue;
+          const int cls = class_index(gx.la, gx.lb, gy.la, gy.lb);
+          if (!fam_active(cls)) continue;
+          gps.push_back(GP{X, Y, cls, true, static_cast<long long>(gx.K) * gy.K, (gx.nm - 1) * 2 + (gy.nm - 1)});
+        }
+    }
     std::stable_sort(gps.begin(), gps.end(), [](const GP& a, const GP& b) {
       if (a.cls != b.cls) return a.cls < b.cls;
+      if (a.fam != b.fam) return b.fam;
+      if (a.seg != b.seg) return a.seg < b.seg;
       return a.cost > b.cost;
     });
     items.clear();
@@ -554,11 +736,15 @@ struct eritile_gpu {
     model_flops = 0.0;
     for (size_t s = 0; s < gps.size();) {
       const int cls = gps[s].cls;
-      ClassWork cw{cls, static_cast<long long>(items.size()), 0, 0, 0, 0.0, 0.0};
+      const bool fam = gps[s].fam;
+      ClassWork cw{cls, fam, static_cast<long long>(items.size()), 0, {0, 0, 0, 0, 0}, 0, 0, 0.0, 0.0};
       long long counter = 0;  // warp-task counter within the class (sharding)
-      for (; s < gps.size() && gps[s].cls == cls; ++s) {
-        const Group& gx = groups[gps[s].X];
-        const Group& gy = groups[gps[s].Y];
+      int cur_seg = 0;
+      for (; s < gps.size() && gps[s].cls == cls && gps[s].fam == fam; ++s) {
+        while (cur_seg < gps[s].seg) cw.seg[++cur_seg] = static_cast<long long>(items.size()) - cw.off;
+        const Group& gx = fam ? ugroups[gps[s].X] : groups[gps[s].X];
+        const Group& gy = fam ? ugroups[gps[s].Y] : groups[gps[s].Y];
+        const std::vector<double>& QQ = fam ? uQ : Q;
         const bool same = gps[s].X == gps[s].Y;
         const int cbase = static_cast<int>(cnt.size());
         long long total = 0;
@@ -567,11 +753,11 @@ struct eritile_gpu {
           long long n = gy.count;
           if (t > 0.0) {
             // survivors: prefix of the Q-descending ket group
-            const double qx = Q[x];
+            const double qx = QQ[x];
             int lo = 0, hi = gy.count;
             while (lo < hi) {
               const int mid = (lo + hi) >> 1;
-              if (qx * Q[gy.first + mid] >= t) lo = mid + 1;
+              if (qx * QQ[gy.first + mid] >= t) lo = mid + 1;
               else hi = mid;
             }
             n = lo;
@@ -581,7 +767,7 @@ struct eritile_gpu {
           total += n;
         }
         cnt.push_back(0);  // sentinel
-        // cut the flat sequence into warp tasks of 32 quartets
+        // cut the flat sequence into warp tasks of 32 (unit) quartets
         int r = 0;      // current bra rank within gx
         long long off = 0;  // offset within bra r's survivors
         for (long long base = 0; base < total; base += 32, ++counter) {
@@ -592,28 +778,39 @@ struct eritile_gpu {
           const int nq = static_cast<int>(std::min<long long>(32, total - base));
           if (counter % nranks == rank) {
             items.push_back(WorkItem{gx.first + r, static_cast<int>(off) | (nq << 24), cbase + r, gy.first});
-            cw.quartets += nq;
             cw.prim_quartets += static_cast<long long>(nq) * gx.K * gy.K;
+            if (!fam) {
+              cw.quartets += nq;
+            } else {  // member quartets of these nq unit pairs
+              int rr = r, oo = static_cast<int>(off);
+              for (int l = 0; l < nq; ++l, ++oo) {
+                while (oo >= cnt[cbase + rr]) {
+                  oo -= cnt[cbase + rr];
+                  ++rr;
+                }
+                cw.quartets += unit_pair_quartets(gx.first + rr, gy.first + oo, t);
+              }
+            }
           }
           off += 32;
         }
       }
       cw.n = static_cast<long long>(items.size()) - cw.off;
+      while (cur_seg < 4) cw.seg[++cur_seg] = cw.n;
       if (cw.n > 0) {
         const ClassEntry& ce = kClassTable[cls];
         const double nv = static_cast<double>((ce.la + 1) * (ce.la + 2) / 2 * (ce.lb + 1) * (ce.lb + 2) / 2 *
                                               (ce.lc + 1) * (ce.lc + 2) / 2 * (ce.ld + 1) * (ce.ld + 2) / 2);
         // F_c = Nprim (42 + 3m + 2(P+B+X)) + Nq (2H + 12 n), with
-        // P, B, X, H from the plan this kernel executes.
+        // P, B, X, H from the plan this kernel executes; Nprim counts the
+        // primitive quartets actually evaluated (once per unit pair).
         cw.flops = static_cast<double>(cw.prim_quartets) *
                        (42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract)) +
                    static_cast<double>(cw.quartets) * (2.0 * ce.hrr_terms + 12.0 * nv);
-        model_flops += cw.flops;
-        quartets += cw.quartets;
-        prim_quartets += cw.prim_quartets;
         work.push_back(cw);
       }
     }
+    update_totals();
     if (!host_only) {
       d_cnt.upload(cnt);
       d_items.upload(items);
@@ -641,6 +838,7 @@ struct eritile_gpu {
     }
     for (size_t w = 0; w < work.size(); ++w) {
       const ClassWork& cw = work[w];
+      if (!active(cw)) continue;
       if (profiling) CK(cudaEventRecord(prof_ev[2 * w], st));
       LaunchArgs a = class_args(cw, dDs, dJK, st);
       kClassTable[cw.cls].var[variant(cw.cls)](a);
@@ -653,8 +851,9 @@ struct eritile_gpu {
   // Per-class device times of the last launch_all (profiling mode).
   void collect_profile() {
     if (!profiling) return;
-    CK(cudaEventSynchronize(prof_ev[2 * work.size() - 1]));
-    for (size_t w = 0; w < work.size(); ++w) work[w].last_ms = elapsed(prof_ev[2 * w], prof_ev[2 * w + 1]);
+    CK(cudaStreamSynchronize(stream));
+    for (int w : active_work()) CK(cudaEventSynchronize(prof_ev[2 * w + 1]));
+    for (int w : active_work()) work[w].last_ms = elapsed(prof_ev[2 * w], prof_ev[2 * w + 1]);
   }
 
   void prescale(const double* dD, double* dDs, cudaStream_t st) {
@@ -858,19 +1057,35 @@ long long eritile_gpu_quartets(const eritile_gpu* ctx, int* xs, int* ys, long lo
   if (!ctx || !ctx->have_lists) return -1;
   std::vector<std::pair<int, int>> q;
   q.reserve(static_cast<size_t>(ctx->quartets));
-  for (const WorkItem& it : ctx->items) {
-    const int nq = it.r0nq >> 24;
-    for (int l = 0; l < nq; ++l) {
-      int qq = (it.r0nq & 0xffffff) + l, x = it.bra0, c = it.cntp;
-      while (qq >= ctx->cnt[c]) {
-        qq -= ctx->cnt[c];
-        ++x;
-        ++c;
+  for (const ClassWork& cw : ctx->work)
+    for (long long w = cw.off; w < (ctx->active(cw) ? cw.off + cw.n : cw.off); ++w) {
+      const WorkItem& it = ctx->items[w];
+      const int nq = it.r0nq >> 24;
+      for (int l = 0; l < nq; ++l) {
+        int qq = (it.r0nq & 0xffffff) + l, x = it.bra0, c = it.cntp;
+        while (qq >= ctx->cnt[c]) {
+          qq -= ctx->cnt[c];
+          ++x;
+          ++c;
+        }
+        const int y = it.yfirst + qq;
+        if (!cw.fam) {
+          const int rx = ctx->pm[x].ref, ry = ctx->pm[y].ref;
+          q.emplace_back(std::min(rx, ry), std::max(rx, ry));
+          continue;
+        }
+        const UnitMeta& a = ctx->um[x];
+        const UnitMeta& b = ctx->um[y];
+        for (int m = 0; m < a.nm; ++m)
+          for (int n = 0; n < b.nm; ++n) {
+            if (x == y && m > n) continue;
+            const int px = m ? a.m1 : a.m0, py = n ? b.m1 : b.m0;
+            if (ctx->tau > 0.0 && ctx->Q[px] * ctx->Q[py] < ctx->tau) continue;
+            const int rx = ctx->pm[px].ref, ry = ctx->pm[py].ref;
+            q.emplace_back(std::min(rx, ry), std::max(rx, ry));
+          }
       }
-      const int rx = ctx->pm[x].ref, ry = ctx->pm[it.yfirst + qq].ref;
-      q.emplace_back(std::min(rx, ry), std::max(rx, ry));
     }
-  }
   std::sort(q.begin(), q.end());
   const long long n = static_cast<long long>(q.size());
   if (xs && ys)
@@ -1049,17 +1264,18 @@ int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, 
   if (!ctx) return ERITILE_ERR_ARG;
   int rc = guard(ctx, [&] { ctx->collect_profile(); });
   if (rc != ERITILE_OK) return rc;
-  const int n = static_cast<int>(ctx->work.size());
-  for (int w = 0; w < std::min(n, cap); ++w) {
-    const ClassWork& cw = ctx->work[w];
+  const std::vector<int> act = ctx->active_work();
+  const int n = static_cast<int>(act.size());
+  for (int k = 0; k < std::min(n, cap); ++k) {
+    const ClassWork& cw = ctx->work[act[k]];
     const ClassEntry& ce = kClassTable[cw.cls];
     if (cls4) {
-      cls4[4 * w] = ce.la; cls4[4 * w + 1] = ce.lb; cls4[4 * w + 2] = ce.lc; cls4[4 * w + 3] = ce.ld;
+      cls4[4 * k] = ce.la; cls4[4 * k + 1] = ce.lb; cls4[4 * k + 2] = ce.lc; cls4[4 * k + 3] = ce.ld;
     }
-    if (ms) ms[w] = cw.last_ms;
-    if (flops) flops[w] = cw.flops;
-    if (quartets) quartets[w] = cw.quartets;
-    if (prim_quartets) prim_quartets[w] = cw.prim_quartets;
+    if (ms) ms[k] = cw.last_ms;
+    if (flops) flops[k] = cw.flops;
+    if (quartets) quartets[k] = cw.quartets;
+    if (prim_quartets) prim_quartets[k] = cw.prim_quartets;
   }
   return n;
 }
@@ -1069,7 +1285,7 @@ int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out) {
   out->nbf = ctx->nbf;
   out->nshells = static_cast<int>(ctx->shells.size());
   out->npairs = static_cast<int>(ctx->pm.size());
-  out->nclasses = static_cast<int>(ctx->work.size());
+  out->nclasses = static_cast<int>(ctx->active_work().size());
   out->quartets = ctx->quartets;
   out->prim_quartets = ctx->prim_quartets;
   out->work_items = static_cast<long long>(ctx->items.size());
@@ -1095,24 +1311,45 @@ int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps) {
 
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms) {
   if (!ctx) return ERITILE_ERR_ARG;
-  const int n = static_cast<int>(ctx->work.size());
-  if (ctx->tune_ms.size() != ctx->work.size() * kMaxVariants) return 0;
-  for (int w = 0; w < std::min(n, cap); ++w) {
-    if (cls_index) cls_index[w] = ctx->work[w].cls;
+  if (ctx->tune_ms.size() != static_cast<size_t>(kNumClasses) * kMaxVariants) return 0;
+  std::vector<int> cl;
+  for (int c = 0; c < kNumClasses; ++c)
+    for (int v = 0; v < kMaxVariants; ++v)
+      if (ctx->tune_ms[static_cast<size_t>(c) * kMaxVariants + v] > 0.0) {
+        cl.push_back(c);
+        break;
+      }
+  const int n = static_cast<int>(cl.size());
+  for (int k = 0; k < std::min(n, cap); ++k) {
+    if (cls_index) cls_index[k] = cl[k];
     if (ms)
-      for (int v = 0; v < kMaxVariants; ++v) ms[w * kMaxVariants + v] = ctx->tune_ms[w * kMaxVariants + v];
+      for (int v = 0; v < kMaxVariants; ++v)
+        ms[k * kMaxVariants + v] = ctx->tune_ms[static_cast<size_t>(cl[k]) * kMaxVariants + v];
   }
   return n;
 }
 
 int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var) {
   if (!ctx || cls_index < 0 || cls_index >= kNumClasses) return ERITILE_ERR_ARG;
-  if (var < 0 || var >= kClassTable[cls_index].nvar) return fail(ctx, ERITILE_ERR_ARG, "no such kernel variant");
-  if (ctx->var_choice.empty()) {
-    ctx->var_choice.resize(kNumClasses);
-    for (int c = 0; c < kNumClasses; ++c) ctx->var_choice[c] = kClassTable[c].def;
-  }
+  if (var < ctx->var_lo(cls_index) || var >= ctx->var_hi(cls_index))
+    return fail(ctx, ERITILE_ERR_ARG, "kernel variant not available (families on: fam_* only)");
+  if (ctx->var_choice.empty()) ctx->var_choice.assign(kNumClasses, -1);
   ctx->var_choice[cls_index] = var;
+  ctx->update_totals();
+  return ERITILE_OK;
+}
+
+int eritile_gpu_set_families(eritile_gpu* ctx, int on) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  ctx->families = on != 0;
+  ctx->have_lists = false;
+  return ERITILE_OK;
+}
+
+int eritile_gpu_variant_range(const eritile_gpu* ctx, int cls_index, int* lo, int* hi) {
+  if (!ctx || cls_index < 0 || cls_index >= kNumClasses || !lo || !hi) return ERITILE_ERR_ARG;
+  *lo = ctx->var_lo(cls_index);
+  *hi = ctx->var_hi(cls_index);
   return ERITILE_OK;
 }
 

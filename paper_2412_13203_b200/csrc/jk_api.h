@@ -39,6 +39,16 @@ constexpr int kBoysRows = 641;    // T_i = i/16, T < 40
 constexpr double kBoysTmax = 40.0;
 constexpr int kBoysMmax = 16;     // slices M = 0..16 (L <= 4)
 
+// A unit of <= 2 product pairs whose primitive-pair records are identical
+// except the contraction weight U (generally contracted sibling shells,
+// csrc/jk_family.cuh). Records are those of member m0; uw[prim] holds
+// (U of m0, U of m1 or 0) per primitive.
+struct alignas(16) UnitMeta {
+  int prim_off, K, nm, pad;
+  int m0, m1, pad1, pad2;  // member product pair ids
+  double ABx, ABy, ABz, pad3;
+};
+
 struct LaunchArgs {
   int mode;  // 0 = J/K digestion, 1 = Schwarz diagonal, 2 = raw quartets
   const WorkItem* items;
@@ -60,6 +70,12 @@ struct LaunchArgs {
   cudaStream_t stream;
   int grid;   // 0 = auto
   int block;  // threads per CTA
+  // family (unit) launches: work items index units
+  const UnitMeta* um;
+  const double2* uw;     // per primitive: member weights
+  const double* Qp;      // Schwarz Q per product pair
+  double tau;            // screening threshold (<= 0: none)
+  long long seg[5];      // unit launches: item offsets of the (1,1) (1,2) (2,1) (2,2) member segments
 };
 
 using LaunchFn = void (*)(const LaunchArgs&);
@@ -67,13 +83,15 @@ using LaunchFn = void (*)(const LaunchArgs&);
 // One canonical ERI class and its kernel variants (straight-line lane
 // kernels at several residency targets and/or the CTA-cooperative table
 // kernel); `def` is the variant used until the allocator tunes the class.
-constexpr int kMaxVariants = 12;
+constexpr int kMaxVariants = 16;
 struct ClassEntry {
   int la, lb, lc, ld, max_m, ops, prim_terms, base, contract, hrr_terms;
   int nvar;
   LaunchFn var[kMaxVariants];
   const char* var_name[kMaxVariants];
   int def;
+  int nfam;     // the last nfam variants are unit ("fam_") kernels
+  int fam_def;  // default unit variant (absolute index), -1 if none
 };
 
 extern const ClassEntry kClassTable[];

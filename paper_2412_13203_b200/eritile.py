@@ -85,6 +85,8 @@ def _lib():
         "eritile_gpu_tune": (C.c_int, [C.c_void_p, _dp, C.c_int]),
         "eritile_gpu_set_variant": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
         "eritile_gpu_tune_times": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+        "eritile_gpu_set_families": (C.c_int, [C.c_void_p, C.c_int]),
+        "eritile_gpu_variant_range": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "eritile_gpu_get_variant": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_class_nvariants": (C.c_int, [C.c_int]),
         "eritile_gpu_variant_name": (C.c_char_p, [C.c_int, C.c_int]),
@@ -294,6 +296,17 @@ class Engine:
         self._check(self._lib.eritile_gpu_tune(self._h, D, int(reps)))
         return self
 
+    def set_families(self, on: bool = True) -> "Engine":
+        """Shared-primitive units for generally contracted sibling shells
+        (csrc/jk_family.cuh); takes effect at the next set_screening."""
+        self._check(self._lib.eritile_gpu_set_families(self._h, int(on)))
+        return self
+
+    def variant_range(self, cls_index: int):
+        lo, hi = C.c_int(), C.c_int()
+        self._check(self._lib.eritile_gpu_variant_range(self._h, int(cls_index), C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
     def set_variant(self, cls_index: int, var) -> "Engine":
         if isinstance(var, str):
             var = variant_names(cls_index).index(var)
@@ -304,13 +317,13 @@ class Engine:
         """{class: {variant name: median ms}} of the last tune."""
         n = self._lib.eritile_gpu_tune_times(self._h, 0, None, None)
         ci = np.zeros(max(n, 1), np.int32)
-        ms = np.zeros(12 * max(n, 1))
+        ms = np.zeros(16 * max(n, 1))
         self._lib.eritile_gpu_tune_times(self._h, n, ci.ctypes.data, ms.ctypes.data)
         tab = class_table()
         out = {}
         for w in range(n):
             names = variant_names(int(ci[w]))
-            out["".join(map(str, tab[ci[w]][:4]))] = {nm: round(float(ms[12 * w + v]), 4) for v, nm in enumerate(names)}
+            out["".join(map(str, tab[ci[w]][:4]))] = {nm: round(float(ms[16 * w + v]), 4) for v, nm in enumerate(names) if ms[16 * w + v] > 0}
         return out
 
     def variants(self) -> dict:

@@ -144,3 +144,31 @@ int main() {
                     "-leritile_b200", "-Wl,-rpath," + str(lib), "-o", str(exe)], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("tau,kappa", [(1e-10, 0.0), (1e-10, 1e-14), (0.0, 1e-14)])
+def test_family_units_keep_the_quartet_list(tau, kappa):
+    """Shared-primitive units (generally contracted sibling shells) change
+    only how many primitive quartets are evaluated: the canonical screened
+    quartet list and its count are identical with units on and off."""
+    from paper_2412_13203_b200.eritile import Engine
+    xyz, bas = geom("w8"), BASIS["cc-pvdz"]
+    O = Oracle("orc").system(xyz, bas, kappa_screen=kappa)
+    Q = O.schwarz()
+    out = {}
+    for fam in (False, True):
+        e = Engine(-1).load_molecule(xyz, bas).build_pairs(kappa)
+        e.set_families(fam)
+        e.set_schwarz(Q)
+        e.set_screening(tau)
+        if fam:  # run every class that has unit kernels on them
+            from paper_2412_13203_b200.eritile import class_table, variant_names
+            for i in range(len(class_table())):
+                names = variant_names(i)
+                if any(n.startswith("fam_") for n in names):
+                    e.set_variant(i, next(k for k, n in enumerate(names) if n.startswith("fam_")))
+        xs, ys = e.quartets()
+        out[fam] = (xs, ys, e.num_quartets(), e.stats()["prim_quartets"])
+    assert np.array_equal(out[True][0], out[False][0]) and np.array_equal(out[True][1], out[False][1])
+    assert out[True][2] == out[False][2] == len(out[True][0])
+    assert out[True][3] < 0.8 * out[False][3]  # O 1s/2s share their nine exponents

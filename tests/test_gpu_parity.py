@@ -153,14 +153,14 @@ def test_dense_reference_loop_water(gpu):
 
 
 def _force_variant(e, k):
-    """Set every class to its k-th kernel variant (clamped)."""
-    from paper_2412_13203_b200.eritile import class_table, variant_names
+    """Set every class to its k-th active kernel variant (clamped)."""
+    from paper_2412_13203_b200.eritile import class_table
     for i in range(len(class_table())):
-        names = variant_names(i)
-        e.set_variant(i, min(k, len(names) - 1))
+        lo, hi = e.variant_range(i)
+        e.set_variant(i, lo + min(k, hi - lo - 1))
 
 
-@pytest.mark.parametrize("k", list(range(12)))
+@pytest.mark.parametrize("k", list(range(16)))
 def test_every_kernel_variant_eri_and_jk(gpu, k):
     """Every kernel variant (lane_m2 / lane_m3 / coop) of every class gives the
     oracle's integrals and J/K (benzene 6-31G* covers all L<=2 classes that
@@ -244,3 +244,34 @@ def test_f_shells_cc_pvtz(gpu, k):
     Jo, Ko, nq = O.build_jk(D, 1e-12)
     assert nq == e.num_quartets()
     assert np.max(np.abs(J - Jo)) < 1e-10 and np.max(np.abs(K - Ko)) < 1e-10
+
+
+@pytest.mark.parametrize("mol,basis,tau,kappa", [("w4", "cc-pvdz", 1e-10, 0.0), ("w8", "cc-pvdz", 1e-10, 1e-14),
+                                                 ("benzene", "6-31g*", 1e-12, 0.0)])
+def test_family_units_jk_match_pairs_and_oracle(gpu, mol, basis, tau, kappa):
+    """Shared-primitive unit kernels give the oracle's J/K (1e-10) and the
+    pair kernels' J/K, with identical quartet lists."""
+    from paper_2412_13203_b200.eritile import Engine
+    xyz, bas = geom(mol), BASIS[basis]
+    D = _rand_density(Engine_k(xyz, bas, kappa, tau).nbf, 9)
+    res = {}
+    for fam in (False, True):
+        e = Engine(0).load_molecule(xyz, bas).build_pairs(kappa)
+        e.set_families(fam)
+        e.set_screening(tau)
+        if fam:  # unit kernels for every class that has them
+            from paper_2412_13203_b200.eritile import class_table, variant_names
+            for i in range(len(class_table())):
+                names = variant_names(i)
+                if any(n.startswith("fam_") for n in names):
+                    e.set_variant(i, next(k for k, n in enumerate(names) if n.startswith("fam_")))
+        res[fam] = (e.build_jk(D), e.quartets(), e.stats()["prim_quartets"])
+    (Jf, Kf), (xf, yf), pf = res[True]
+    (Jp, Kp), (xp, yp), pp = res[False]
+    assert np.array_equal(xf, xp) and np.array_equal(yf, yp)
+    if mol.startswith("w"):
+        assert pf < pp  # O 1s/2s primitive quartets evaluated once
+    assert np.max(np.abs(Jf - Jp)) < 1e-11 and np.max(np.abs(Kf - Kp)) < 1e-11
+    Jo, Ko, nq = Oracle("orc").system(xyz, bas, kappa_screen=kappa).build_jk(D, tau)
+    assert nq == len(xf)
+    assert np.max(np.abs(Jf - Jo)) < 1e-10 and np.max(np.abs(Kf - Ko)) < 1e-10
