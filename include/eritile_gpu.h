@@ -145,6 +145,8 @@ int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var);
  * "fam_" variants then run only those. Takes effect at the next
  * set_screening. Results and quartet lists are unchanged. */
 int eritile_gpu_set_families(eritile_gpu* ctx, int on);
+/* Class launches of a build on 4 streams (default) or on one stream. */
+int eritile_gpu_set_concurrent(eritile_gpu* ctx, int on);
 /* Active variant index range [lo, hi) of a class in this context. */
 int eritile_gpu_variant_range(const eritile_gpu* ctx, int cls_index, int* lo, int* hi);
 int eritile_gpu_get_variant(const eritile_gpu* ctx, int cls_index);

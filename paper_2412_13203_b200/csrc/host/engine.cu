@@ -275,7 +275,18 @@ struct eritile_gpu {
   bool host_only = false;  // device < 0: block constructor / lists only
   std::vector<cudaEvent_t> prof_ev;
 
+  static constexpr int kSide = 3;
+  bool concurrent = true;
+  cudaStream_t side[kSide] = {nullptr, nullptr, nullptr};
+  cudaEvent_t side_ev[kSide] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr;
+
   ~eritile_gpu() {
+    for (int k = 0; k < kSide; ++k) {
+      if (side[k]) cudaStreamDestroy(side[k]);
+      if (side_ev[k]) cudaEventDestroy(side_ev[k]);
+    }
+    if (fork_ev) cudaEventDestroy(fork_ev);
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -836,15 +847,45 @@ struct eritile_gpu {
         prof_ev.push_back(e);
       }
     }
-    for (size_t w = 0; w < work.size(); ++w) {
-      const ClassWork& cw = work[w];
-      if (!active(cw)) continue;
-      if (profiling) CK(cudaEventRecord(prof_ev[2 * w], st));
-      LaunchArgs a = class_args(cw, dDs, dJK, st);
+    if (profiling || !concurrent) {  // one stream: per-class events are exact
+      for (size_t w = 0; w < work.size(); ++w) {
+        const ClassWork& cw = work[w];
+        if (!active(cw)) continue;
+        if (profiling) CK(cudaEventRecord(prof_ev[2 * w], st));
+        LaunchArgs a = class_args(cw, dDs, dJK, st);
+        kClassTable[cw.cls].var[variant(cw.cls)](a);
+        CK(cudaGetLastError());
+        ++launches_last;
+        if (profiling) CK(cudaEventRecord(prof_ev[2 * w + 1], st));
+      }
+      return;
+    }
+    // Class launches are independent (commutative FP64 reductions into J/K):
+    // heaviest first, dealt over kSide+1 streams so each launch's last wave
+    // overlaps the next launch instead of idling SMs. Forked from / joined
+    // back to `st` with events.
+    if (side[0] == nullptr) {
+      for (int k = 0; k < kSide; ++k) {
+        CK(cudaStreamCreateWithFlags(&side[k], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&side_ev[k], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    }
+    std::vector<int> act = active_work();
+    std::stable_sort(act.begin(), act.end(), [&](int a, int b) { return work[a].flops > work[b].flops; });
+    CK(cudaEventRecord(fork_ev, st));
+    for (int k = 0; k < kSide; ++k) CK(cudaStreamWaitEvent(side[k], fork_ev, 0));
+    for (size_t i = 0; i < act.size(); ++i) {
+      const ClassWork& cw = work[act[i]];
+      cudaStream_t s = (i % (kSide + 1) == 0) ? st : side[i % (kSide + 1) - 1];
+      LaunchArgs a = class_args(cw, dDs, dJK, s);
       kClassTable[cw.cls].var[variant(cw.cls)](a);
       CK(cudaGetLastError());
       ++launches_last;
-      if (profiling) CK(cudaEventRecord(prof_ev[2 * w + 1], st));
+    }
+    for (int k = 0; k < kSide; ++k) {
+      CK(cudaEventRecord(side_ev[k], side[k]));
+      CK(cudaStreamWaitEvent(st, side_ev[k], 0));
     }
   }
 
@@ -1336,6 +1377,12 @@ int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var) {
   if (ctx->var_choice.empty()) ctx->var_choice.assign(kNumClasses, -1);
   ctx->var_choice[cls_index] = var;
   ctx->update_totals();
+  return ERITILE_OK;
+}
+
+int eritile_gpu_set_concurrent(eritile_gpu* ctx, int on) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  ctx->concurrent = on != 0;
   return ERITILE_OK;
 }
 

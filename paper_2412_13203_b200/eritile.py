@@ -86,6 +86,7 @@ def _lib():
         "eritile_gpu_set_variant": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
         "eritile_gpu_tune_times": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
         "eritile_gpu_set_families": (C.c_int, [C.c_void_p, C.c_int]),
+        "eritile_gpu_set_concurrent": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_variant_range": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "eritile_gpu_get_variant": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_class_nvariants": (C.c_int, [C.c_int]),
@@ -300,6 +301,11 @@ class Engine:
         """Shared-primitive units for generally contracted sibling shells
         (csrc/jk_family.cuh); takes effect at the next set_screening."""
         self._check(self._lib.eritile_gpu_set_families(self._h, int(on)))
+        return self
+
+    def set_concurrent(self, on: bool = True) -> "Engine":
+        """Class launches on 4 streams (default) or serialised on one."""
+        self._check(self._lib.eritile_gpu_set_concurrent(self._h, int(on)))
         return self
 
     def variant_range(self, cls_index: int):
