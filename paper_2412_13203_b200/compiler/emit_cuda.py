@@ -285,8 +285,8 @@ def variants(info) -> List[Tuple[str, str]]:
         # engine uses these (and only these) when families are enabled
         out.append(("fam_pl512", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512>"))
         out.append(("fam_pl768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 768>"))
-        out.append(("fam_pf512", f"launch_fam<Cls{cid}, 1, kLoopPrefetch, 512>"))
-        out.append(("fam_m2", f"launch_fam<Cls{cid}, 2, kLoopPlain, 256>"))
+        out.append(("fam_x768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 768>"))
+        out.append(("fam_x1024", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 1024>"))
     assert len(out) <= 16, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 

@@ -229,14 +229,16 @@ void launch_fam_seg(const LaunchArgs& a, long long i0, long long i1) {
   jk_fam_kernel<C, MB, MK, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a, i0, i1);
 }
 
-template <class C, int MINB, int STYLE, int NT>
+// NT11: CTA size of the (1,1) segment (fewest live accumulators: it fits
+// the tighter register budget of larger CTAs).
+template <class C, int MINB, int STYLE, int NT, int NT11 = NT>
 void launch_fam(const LaunchArgs& a) {
   if (a.mode != 0) {  // Schwarz / raw quartets are per pair: the lane kernel serves them
     launch_class<C, 2, kLoopPrefetch>(a);
     return;
   }
   // segments (1,1) (1,2) (2,1) (2,2) of the class's items
-  launch_fam_seg<C, 1, 1, MINB, STYLE, NT>(a, a.seg[0], a.seg[1]);
+  launch_fam_seg<C, 1, 1, MINB, STYLE, NT11>(a, a.seg[0], a.seg[1]);
   launch_fam_seg<C, 1, 2, MINB, STYLE, NT>(a, a.seg[1], a.seg[2]);
   launch_fam_seg<C, 2, 1, MINB, STYLE, NT>(a, a.seg[2], a.seg[3]);
   launch_fam_seg<C, 2, 2, MINB, STYLE, NT>(a, a.seg[3], a.seg[4]);
