@@ -333,7 +333,8 @@ def run_ours(args, rank, nranks, local_rank):
     if top:
         ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": traffic, "kernel": "jk_kernel<Cls%d%d%d%d>" % top["cls"],
+                "traffic": traffic,
+                "kernel": "class (%d%d%d%d) launch, variant %s" % (*top["cls"], chosen.get(tuple(top["cls"]))),
                 "kernel_share_of_build": top["ms"] / total_prof_ms,
                 "build_frac": (fl_tot / (ms * 1e-3) / 1e12) / (peak * nranks),
                 "peak_source": peak_src,
