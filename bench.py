@@ -28,7 +28,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-METRIC = "Fock-build ERI quartets/s ((H2O)_{waters} {basis}, Schwarz tau={tau:g})"
+METRIC = "Fock-build ERI quartets/s ({mol} {basis}, Schwarz tau={tau:g})"
 UNIT = "quartets/s"
 
 
@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--waters", type=int, default=80)
     ap.add_argument("--basis", default="cc-pvdz")
+    ap.add_argument("--geom", default="", help="geometry fixture (e.g. benzene) instead of the water cluster")
     ap.add_argument("--tau", type=float, default=1e-10)
     ap.add_argument("--kappa", type=float, default=1e-14,
                     help="reference primitive-pair screen |coef|*kappa < thr (block.hpp:83-89; "
@@ -57,7 +58,8 @@ BASIS_FILES = {"sto-3g": "sto-3g.txt", "6-31g*": "6-31gs.txt", "cc-pvdz": "cc-pv
 def workload(args):
     from paper_2412_13203_b200.eritile import read_fixture
     from paper_2412_13203_b200.geometry import water_cluster
-    return water_cluster(args.waters), read_fixture("basis", BASIS_FILES[args.basis])
+    xyz = read_fixture("geom", args.geom + ".xyz") if args.geom else water_cluster(args.waters)
+    return xyz, read_fixture("basis", BASIS_FILES[args.basis])
 
 
 def synthetic_density(N: int, nocc: int, seed: int = 2412) -> np.ndarray:
@@ -67,7 +69,8 @@ def synthetic_density(N: int, nocc: int, seed: int = 2412) -> np.ndarray:
 
 
 def config(args, nranks):
-    return {"workload": f"(H2O)_{args.waters}/{args.basis} RHF Fock build (ERI + J/K), Schwarz tau={args.tau:g}, "
+    mol = args.geom if args.geom else f"(H2O)_{args.waters}"
+    return {"workload": f"{mol}/{args.basis} RHF Fock build (ERI + J/K), Schwarz tau={args.tau:g}, "
                         f"kappa screen {args.kappa:g}",
             "n_basis": None, "tau": args.tau, "kappa_screen": args.kappa, "basis": args.basis, "waters": args.waters,
             "density": "synthetic C_occ C_occ^T (seeded QR)", "parallelism": f"quartet-shard x{nranks} + NCCL allreduce(J,K)",
@@ -340,7 +343,7 @@ def run_ours(args, rank, nranks, local_rank):
                 "peak_source": peak_src,
                 "flops_model": "SURVEY.md 8d: F_c = Nprim(42+3m+2(P+B+X)) + Nq(2H+12n), executed plan"}
     out = {
-        "metric": METRIC.format(waters=args.waters, basis=args.basis, tau=args.tau), "value": q_tot / (ms * 1e-3), "unit": UNIT, "n_gpus": nranks, "steps": args.steps,
+        "metric": METRIC.format(mol=args.geom or f"(H2O)_{args.waters}", basis=args.basis, tau=args.tau), "value": q_tot / (ms * 1e-3), "unit": UNIT, "n_gpus": nranks, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic water-cluster geometry, seeded density)",
         "config": dict(config(args, nranks), n_basis=N),
@@ -378,7 +381,7 @@ def run_reference(args, rank):
     if rank != 0:
         return None
     cb = cpu_sample(args, steps=args.steps, warmup=args.warmup, target_s=args.cpu_seconds, reference_arm=True)
-    return {"metric": METRIC.format(waters=args.waters, basis=args.basis, tau=args.tau), "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    return {"metric": METRIC.format(mol=args.geom or f"(H2O)_{args.waters}", basis=args.basis, tau=args.tau), "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic water-cluster geometry, seeded density)",
             "config": dict(config(args, 1), n_basis=cb["n_basis"]), "impl": "reference",

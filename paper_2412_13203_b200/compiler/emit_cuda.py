@@ -253,6 +253,7 @@ COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2, 3)
 COOP_SMEM_BUDGET = 110 * 1024
+COOPW_MAX_SLOTS = 6000  # 4 warps x (slots + 112) doubles <= ~196 KB
 FAM_MAX_BOUNDARY = int(os.environ.get("ERITILE_FAM_MAX_BOUNDARY", "9"))  # keep >= 2 CTAs/SM when the Boys slice is staged
 
 
@@ -280,6 +281,8 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("lane_pl1024", f"launch_class<Cls{cid}, 1, kLoopPlain, 1024>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
+        if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:
+            out.append(("coopw", f"launch_coopw_cls{cid}"))
     if info["boundary"] <= FAM_MAX_BOUNDARY:
         # shared-primitive unit kernels (csrc/jk_family.cuh); kept last: the
         # engine uses these (and only these) when families are enabled
@@ -307,6 +310,9 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         body, info = emit_class(cls)
         cid = class_id(cls)
         info["index"] = idx
+        sc = schedule(cls) if info["ops"] >= COOP_MIN_OPS else None
+        if sc is not None:
+            info["coop_slots"] = sc["nslots"]
         vs = variants(info)
         info["variants"] = vs
         info["default"] = default_variant(info, vs)
@@ -324,7 +330,6 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
                        f"NC = {nc}, ND = {nd};\n  static constexpr int NV = {na * nb * nc * nd};\n"
                        f"  static constexpr int M = {info['M']};\n  static constexpr int OPS = {info['ops']};\n}};")
         if coop:
-            sc = schedule(cls)
             width = max(b - a for a, b in zip(sc["lo_lvl"], sc["lo_lvl"][1:]))
             nt = 256 if width >= 192 else 128
             src.append(emit_tables(cid, sc))
@@ -344,15 +349,28 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
                        f"t.nslots = {sc['nslots']};")
             src.append(f"  launch_coop<CoopCls{cid}>(t, a);")
             src.append("}")
+            if any(n == "coopw" for n, _ in vs):
+                src.append(f"void launch_coopw_cls{cid}(const LaunchArgs& a) {{")
+                src.append("  CoopTables t{};")
+                for fld, sym in [("lo", "kLo"), ("lo_lvl", "kLoLvl"), ("bd", "kBd"), ("up", "kUp"),
+                                 ("up_lvl", "kUpLvl"), ("combo", "kCombo"), ("tgt", "kTgt")]:
+                    src.append(f"  cudaGetSymbolAddress((void**)&t.{fld}, {sym}{cid});")
+                src.append(f"  t.nlo_lvl = {len(sc['lo_lvl']) - 1}; t.nb = {sc['nb']}; "
+                           f"t.nup_lvl = {len(sc['up_lvl']) - 1}; t.ncombo = {len(sc['combo'])}; "
+                           f"t.nslots = {sc['nslots']};")
+                src.append(f"  launch_coopw<CoopCls{cid}>(t, a);")
+                src.append("}")
         for name, expr in vs:
-            if name != "coop":
+            if name not in ("coop", "coopw"):
                 src.append(f"void launch_{name}_cls{cid}(const LaunchArgs& a) {{ {expr}(a); }}")
         src += ["}  // namespace eritile_b200", ""]
         _write_if_changed(outdir / f"cls_{cid}.cu", "\n".join(src))
     reg = ["// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
            '#include "../jk_api.h"', "namespace eritile_b200 {"]
     def fn(name, cid):
-        return f"launch_coop_cls{cid}" if name == "coop" else f"launch_{name}_cls{cid}"
+        if name in ("coop", "coopw"):
+            return f"launch_{name}_cls{cid}"
+        return f"launch_{name}_cls{cid}"
     for info in infos:
         cid = class_id(info["cls"])
         for name, _ in info["variants"]:

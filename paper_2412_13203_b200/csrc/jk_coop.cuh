@@ -266,4 +266,231 @@ void launch_coop(const CoopTables& tb, const LaunchArgs& a) {
   coop_kernel<C><<<grid, C::NT, smem, a.stream>>>(tb, a);
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative form of the same tables: each warp owns one contracted
+// quartet at a time in its own shared-memory slot region, so a level needs
+// only __syncwarp() and a CTA holds kCoopWarps independent quartets (no CTA
+// barriers). Suited to quartets with few primitive quartets (d/f shells are
+// contracted over one primitive in cc-pVXZ), where the CTA form is barrier-
+// and binding-bound. The Boys slice is read through L1 from global memory.
+constexpr int kCoopWarps = 4;
+
+template <class C>
+__device__ __forceinline__ void coopw_eval(const CoopTables& tb, const PairMeta& bm, const PairMeta& km,
+                                           const PrimRec* __restrict__ prims, const double* __restrict__ btab,
+                                           double* coefb, double* cf, double* val, int lane) {
+  for (int s = lane; s < tb.nb; s += 32) val[1 + s] = 0.0;
+  const PrimRec* bra = prims + bm.prim_off;
+  const PrimRec* ket = prims + km.prim_off;
+  const int np = bm.K * km.K;
+  for (int pq = 0; pq < np; ++pq) {
+    __syncwarp();
+    {
+      const PrimRec bp = load_prim<true>(bra + pq / km.K);
+      const PrimRec kp = load_prim<true>(ket + pq % km.K);
+      const double s = bp.p + kp.p;
+      const double rs = rsqrt_pos(s);
+      const double inv = rs * rs;
+      const double PQx = bp.Px - kp.Px, PQy = bp.Py - kp.Py, PQz = bp.Pz - kp.Pz;
+      const double pinv = bp.p * inv, qinv = kp.p * inv;
+      const double rho = bp.p * qinv;
+      const double T = rho * fma(PQx, PQx, fma(PQy, PQy, PQz * PQz));
+      const double pref = bp.U * kp.U * rs;
+      if (lane == 0) {
+        coefb[0] = 1.0;
+        coefb[kB_PA] = bp.PAx; coefb[kB_PA + 1] = bp.PAy; coefb[kB_PA + 2] = bp.PAz;
+        coefb[kB_QC] = kp.PAx; coefb[kB_QC + 1] = kp.PAy; coefb[kB_QC + 2] = kp.PAz;
+        coefb[kB_WP] = -qinv * PQx; coefb[kB_WP + 1] = -qinv * PQy; coefb[kB_WP + 2] = -qinv * PQz;
+        coefb[kB_WQ] = pinv * PQx; coefb[kB_WQ + 1] = pinv * PQy; coefb[kB_WQ + 2] = pinv * PQz;
+      } else if (lane == 1) {
+        coefb[kB_I2P] = bp.i2p;
+        coefb[kB_I2Q] = kp.i2p;
+        coefb[kB_I2PQ] = 0.5 * inv;
+        coefb[kB_ITP] = bp.i2p * qinv;
+        coefb[kB_ITQ] = kp.i2p * pinv;
+        coefb[kB_AB] = bm.ABx; coefb[kB_AB + 1] = bm.ABy; coefb[kB_AB + 2] = bm.ABz;
+        coefb[kB_CD] = km.ABx; coefb[kB_CD + 1] = km.ABy; coefb[kB_CD + 2] = km.ABz;
+      } else if (lane == 2) {
+        double F[C::M + 1];
+        boys_eval<C::M>(T, btab, F);
+#pragma unroll
+        for (int m = 0; m <= C::M; ++m) coefb[kB_PF + m] = pref * F[m];
+      }
+    }
+    __syncwarp();
+    for (int k = lane; k < tb.ncombo; k += 32) {
+      const unsigned w = __ldg(tb.combo + k);
+      cf[k] = static_cast<double>(static_cast<int>(w >> 8) - 128) * coefb[w & 0xff];
+    }
+    __syncwarp();
+    for (int L = 0; L < tb.nlo_lvl; ++L) {
+      const int e = __ldg(tb.lo_lvl + L + 1);
+      for (int o = __ldg(tb.lo_lvl + L) + lane; o < e; o += 32) {
+        const uint4* op = reinterpret_cast<const uint4*>(tb.lo) + 2 * o;
+        const uint4 h = __ldg(op);
+        const int nt = h.x >> 16;
+        double acc = cf[h.y >> 16] * val[h.y & 0xffff];
+        if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
+        if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
+        if (nt > 3) {
+          const uint4 g = __ldg(op + 1);
+          acc = fma(cf[g.x >> 16], val[g.x & 0xffff], acc);
+          if (nt > 4) acc = fma(cf[g.y >> 16], val[g.y & 0xffff], acc);
+        }
+        val[h.x & 0xffff] = acc;
+      }
+      __syncwarp();
+    }
+    for (int k = lane; k < tb.nb; k += 32) {
+      const unsigned w = __ldg(tb.bd + k);
+      val[w >> 16] += val[w & 0xffff];
+    }
+  }
+  __syncwarp();
+  // coefb[kB_AB..] / [kB_CD..] are set per primitive quartet; the
+  // horizontal combos only read UNIT, AB and CD, which are quartet constants
+  for (int L = 0; L < tb.nup_lvl; ++L) {
+    const int e = __ldg(tb.up_lvl + L + 1);
+    for (int o = __ldg(tb.up_lvl + L) + lane; o < e; o += 32) {
+      const uint4 h = __ldg(reinterpret_cast<const uint4*>(tb.up) + o);
+      const int nt = h.x >> 16;
+      double acc = cf[h.y >> 16] * val[h.y & 0xffff];
+      if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
+      if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
+      val[h.x & 0xffff] = acc;
+    }
+    __syncwarp();
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(32 * kCoopWarps) coopw_kernel(CoopTables tb, LaunchArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int region = kCoopBase + kCoopMaxCombo + tb.nslots;
+  double* coefb = smem + static_cast<size_t>(wid) * region;
+  double* cf = coefb + kCoopBase;
+  double* val = cf + kCoopMaxCombo;
+  const double* btab = a.boys_tab + static_cast<size_t>(C::M) * kBoysRows * kBoysCols;
+  if (lane == 0) val[0] = 1.0;
+  __syncwarp();
+  const long long gw = static_cast<long long>(blockIdx.x) * kCoopWarps + wid;
+  const long long nw = static_cast<long long>(gridDim.x) * kCoopWarps;
+  const size_t n = static_cast<size_t>(a.N);
+  constexpr int NA = C::NA, NB = C::NB, NC = C::NC, ND = C::ND;
+  constexpr int O1 = NA * NB, O2 = O1 + NC * ND, O3 = O2 + NA * NC, O4 = O3 + NB * ND, O5 = O4 + NA * ND,
+                O6 = O5 + NB * NC;
+  if (a.mode == 1 || a.mode == 2) {
+    const long long cnt = a.mode == 1 ? a.npair_list : a.nq;
+    for (long long i = gw; i < cnt; i += nw) {
+      const int xb = a.mode == 1 ? a.pair_list[i] : a.qpairs[2 * i];
+      const int xk = a.mode == 1 ? xb : a.qpairs[2 * i + 1];
+      const PairMeta bm = a.pm[xb], km = a.pm[xk];
+      coopw_eval<C>(tb, bm, km, a.prims, btab, coefb, cf, val, lane);
+      if (a.mode == 2) {
+        for (int k = lane; k < C::NV; k += 32) a.qout[i * C::NV + k] = val[__ldg(tb.tgt + k)];
+      } else {
+        double mx = 0.0;
+        for (int ab = lane; ab < NA * NB; ab += 32) {
+          const int ia = ab / NB, ib = ab % NB;
+          const double sc = comp_scale(C::LA, ia) * comp_scale(C::LB, ib);
+          mx = fmax(mx, fabs(val[__ldg(tb.tgt + (ab * NC + ia) * ND + ib)]) * (sc * sc));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) a.Qout[xb] = sqrt(mx);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  for (long long w = gw; w < a.nitems; w += nw) {
+    const WorkItem it = a.items[w];
+    const int nq = it.r0nq >> 24;
+    int q = it.r0nq & 0xffffff, x = it.bra0, c = it.cntp;
+    for (int l = 0; l < nq; ++l, ++q) {
+      for (int cn = __ldg(a.cnt + c); q >= cn; cn = __ldg(a.cnt + c)) {
+        q -= cn;
+        ++x;
+        ++c;
+      }
+      const int y = it.yfirst + q;
+      const PairMeta bm = a.pm[x], km = a.pm[y];
+      coopw_eval<C>(tb, bm, km, a.prims, btab, coefb, cf, val, lane);
+      const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (x != y ? 2.0 : 1.0);
+      const double wj = 0.5 * deg, wk = 0.25 * deg;
+      for (int o = lane; o < O6; o += 32) {
+        double s = 0.0;
+        double* dst;
+        if (o < O1) {
+          const int ia = o / NB, ib = o % NB;
+          for (int ic = 0; ic < NC; ++ic)
+            for (int id = 0; id < ND; ++id)
+              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (km.bfa + ic) * n + km.bfb + id), s);
+          dst = a.J + (bm.bfa + ia) * n + bm.bfb + ib;
+          s *= wj;
+        } else if (o < O2) {
+          const int ic = (o - O1) / ND, id = (o - O1) % ND;
+          for (int ia = 0; ia < NA; ++ia)
+            for (int ib = 0; ib < NB; ++ib)
+              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfa + ia) * n + bm.bfb + ib), s);
+          dst = a.J + (km.bfa + ic) * n + km.bfb + id;
+          s *= wj;
+        } else if (o < O3) {
+          const int ia = (o - O2) / NC, ic = (o - O2) % NC;
+          for (int ib = 0; ib < NB; ++ib)
+            for (int id = 0; id < ND; ++id)
+              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfb + ib) * n + km.bfb + id), s);
+          dst = a.K + (bm.bfa + ia) * n + km.bfa + ic;
+          s *= wk;
+        } else if (o < O4) {
+          const int ib = (o - O3) / ND, id = (o - O3) % ND;
+          for (int ia = 0; ia < NA; ++ia)
+            for (int ic = 0; ic < NC; ++ic)
+              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfa + ia) * n + km.bfa + ic), s);
+          dst = a.K + (bm.bfb + ib) * n + km.bfb + id;
+          s *= wk;
+        } else if (o < O5) {
+          const int ia = (o - O4) / ND, id = (o - O4) % ND;
+          for (int ib = 0; ib < NB; ++ib)
+            for (int ic = 0; ic < NC; ++ic)
+              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfb + ib) * n + km.bfa + ic), s);
+          dst = a.K + (bm.bfa + ia) * n + km.bfb + id;
+          s *= wk;
+        } else {
+          const int ib = (o - O5) / NC, ic = (o - O5) % NC;
+          for (int ia = 0; ia < NA; ++ia)
+            for (int id = 0; id < ND; ++id)
+              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfa + ia) * n + km.bfb + id), s);
+          dst = a.K + (bm.bfb + ib) * n + km.bfa + ic;
+          s *= wk;
+        }
+        red_add(dst, s);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <class C>
+void launch_coopw(const CoopTables& tb, const LaunchArgs& a) {
+  const size_t smem = sizeof(double) * kCoopWarps * (kCoopBase + kCoopMaxCombo + tb.nslots);
+  const long long n = a.mode == 0 ? a.nitems : (a.mode == 1 ? a.npair_list : a.nq);
+  if (n <= 0) return;
+  static int blocks_per_sm = 0, sms = 0;
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(coopw_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, coopw_kernel<C>, 32 * kCoopWarps, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const long long cap = static_cast<long long>(blocks_per_sm) * sms;
+  const long long want = (n + kCoopWarps - 1) / kCoopWarps;
+  const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
+  coopw_kernel<C><<<grid, 32 * kCoopWarps, smem, a.stream>>>(tb, a);
+}
+
 }  // namespace eritile_b200

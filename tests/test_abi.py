@@ -53,7 +53,7 @@ def test_class_table():
         names = variant_names(i)
         assert names and len(set(names)) == len(names)
         if r[5] > 4000:
-            assert names == ["coop"]
+            assert set(names) <= {"coop", "coopw"} and "coop" in names
 
 
 @pytest.mark.parametrize("mol,basis", [("water", "sto-3g"), ("benzene", "6-31g*"), ("w8", "cc-pvdz")])
