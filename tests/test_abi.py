@@ -172,3 +172,25 @@ def test_family_units_keep_the_quartet_list(tau, kappa):
     assert np.array_equal(out[True][0], out[False][0]) and np.array_equal(out[True][1], out[False][1])
     assert out[True][2] == out[False][2] == len(out[True][0])
     assert out[True][3] < 0.8 * out[False][3]  # O 1s/2s share their nine exponents
+
+
+def test_host_edge_cases_lists():
+    """Host Block Constructor edge cases: all quartets screened away, a single
+    shell (one pair, one quartet), and the reference's empty-pair drop under
+    the kappa screen (block.hpp:86-87)."""
+    from paper_2412_13203_b200.eritile import Engine
+    xyz, bas = geom("water"), BASIS["cc-pvdz"]
+    O = Oracle("orc").system(xyz, bas)
+    e = Engine(-1).load_molecule(xyz, bas).build_pairs(0.0)
+    e.set_schwarz(O.schwarz())
+    e.set_screening(1e6)
+    assert e.num_quartets() == 0 and len(e.quartets()[0]) == 0
+    h = "1\nH atom\nH 0.0 0.0 0.0\n"
+    e = Engine(-1).load_molecule(h, BASIS["sto-3g"]).build_pairs(0.0)
+    e.set_screening(0.0)
+    xs, ys = e.quartets()
+    assert (e.npairs, e.num_quartets(), xs.tolist(), ys.tolist()) == (1, 1, [0], [0])
+    far = "2\nfar apart\nH 0 0 0\nH 0 0 40.0\n"
+    e = Engine(-1).load_molecule(far, BASIS["sto-3g"]).build_pairs(1e-14)
+    o = Oracle("orc").system(far, BASIS["sto-3g"], kappa_screen=1e-14)
+    assert e.npairs == o.npairs == 2  # the inter-atomic pair has no primitive left

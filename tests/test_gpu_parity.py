@@ -275,3 +275,22 @@ def test_family_units_jk_match_pairs_and_oracle(gpu, mol, basis, tau, kappa):
     Jo, Ko, nq = Oracle("orc").system(xyz, bas, kappa_screen=kappa).build_jk(D, tau)
     assert nq == len(xf)
     assert np.max(np.abs(Jf - Jo)) < 1e-10 and np.max(np.abs(Kf - Ko)) < 1e-10
+
+
+def test_edge_cases_empty_and_tiny(gpu):
+    """Edge cases: every quartet screened out (J = K = 0, no launches of class
+    kernels), a single-shell system, and H2 (two identical s shells)."""
+    xyz, bas = geom("water"), BASIS["cc-pvdz"]
+    e = _engine(xyz, bas, 1e6)
+    assert e.num_quartets() == 0 and len(e.quartets()[0]) == 0
+    J, K = e.build_jk(_rand_density(e.nbf))
+    assert not J.any() and not K.any()
+    h = "1\nH atom\nH 0.0 0.0 0.0\n"
+    for x, b in [(h, BASIS["sto-3g"]), (geom("h2"), BASIS["sto-3g"]), (geom("h2"), BASIS["cc-pvdz"])]:
+        e = _engine(x, b, 0.0)
+        O = Oracle("orc").system(x, b)
+        D = _rand_density(e.nbf, 2)
+        J, K = e.build_jk(D)
+        Jo, Ko, nq = O.build_jk(D, 0.0)
+        assert nq == e.num_quartets()
+        assert np.max(np.abs(J - Jo)) < 1e-12 and np.max(np.abs(K - Ko)) < 1e-12
