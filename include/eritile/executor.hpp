@@ -48,6 +48,8 @@ class GpuExecutor {
     return q;
   }
   void set_shard(int rank, int nranks) { check(eritile_gpu_set_shard(ctx_, rank, nranks)); }
+  // Workload Allocator: fastest kernel variant per class on D.
+  void tune(const std::vector<double>& D, int reps = 2) { check(eritile_gpu_tune(ctx_, D.data(), reps)); }
   void set_screening(double tau) { check(eritile_gpu_set_screening(ctx_, tau)); }
   int nbf() const { return eritile_gpu_nbf(ctx_); }
 
