@@ -19,7 +19,8 @@ Tables (all little integers, emitted as ``__device__`` arrays):
 * ``combo``: the distinct (coefficient kind, direction, factor) triples of
   the plan, ``base_id | (factor + 128) << 8``; per primitive quartet the CTA
   forms ``factor * coef[base_id]`` once, so every plan term is one FMA;
-* ``tgt``: slot of each output value, kernel a-major order (dag.hpp:221-229).
+* ``tgt``: slot of each output value, kernel a-major order (dag.hpp:221-229);
+  a final copy level places them contiguously when shared memory allows.
 
 Slot allocation is level-aware: a slot read at level L may be rewritten
 from level L+1 on, so ops of one level never race. Slot 0 holds 1.0.
@@ -39,6 +40,9 @@ B_I2P, B_I2Q, B_I2PQ, B_ITP, B_ITQ = 13, 14, 15, 16, 17
 B_AB, B_CD = 18, 21
 B_PF = 24  # pref * F_m, m = 0..M
 MAX_COMBO = 64
+# contiguous output copy level: measured slower (the extra slots cost more
+# occupancy than the indirection saves), off
+COPY_TARGETS = False
 
 
 def _base_id(kind: int, d: int, swap: bool) -> int:
@@ -204,13 +208,27 @@ def schedule(cls) -> Dict:
             up_ops.append([s | (len(terms) << 16)] + [src | (c << 16) for src, c in terms]
                           + [0] * (3 - len(terms)))
         up_lvl.append(len(up_ops))
-    nslots = max(lo_high, ualloc.high, 1 + nb)
+    # final copy level: outputs into a contiguous region [t0, t0 + NV) in
+    # kernel a-major order, so digestion indexes them without indirection
+    # (only when it fits: the largest L=3 plans keep the indirect targets)
+    base_slots = max(lo_high, ualloc.high, 1 + nb)
+    if COPY_TARGETS and base_slots + len(targets) <= 20000:
+        t0 = base_slots
+        unit_combo = combo(UNIT, 0, 1.0)
+        for k, n in enumerate(targets):
+            up_ops.append([(t0 + k) | (1 << 16), uslot[n] | (unit_combo << 16), 0, 0])
+        up_lvl.append(len(up_ops))
+        nslots = t0 + len(targets)
+        tgt = [t0 + k for k in range(len(targets))]
+    else:
+        nslots = base_slots
+        tgt = [uslot[n] for n in targets]
     assert nslots < 65536 and len(combos) <= MAX_COMBO, (cls, nslots, len(combos))
     combo_words = [0] * len(combos)
     for (bid, fac), k in combos.items():
         combo_words[k] = bid | ((fac + 128) << 8)
     return dict(cls=cls, swap=swap, M=M, nslots=nslots, nb=nb, lo=lo_ops, lo_lvl=lo_lvl, bd=bd,
-                up=up_ops, up_lvl=up_lvl, combo=combo_words, tgt=[uslot[n] for n in targets],
+                up=up_ops, up_lvl=up_lvl, combo=combo_words, tgt=tgt,
                 ops=plan.op_count)
 
 

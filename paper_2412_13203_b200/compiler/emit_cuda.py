@@ -253,7 +253,7 @@ COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2, 3)
 COOP_SMEM_BUDGET = 110 * 1024
-COOPW_MAX_SLOTS = 6000  # 4 warps x (slots + 112) doubles <= ~196 KB
+COOPW_MAX_SLOTS = 5500  # 4 warps x (slots + 112) doubles <= ~196 KB
 FAM_MAX_BOUNDARY = int(os.environ.get("ERITILE_FAM_MAX_BOUNDARY", "9"))  # keep >= 2 CTAs/SM when the Boys slice is staged
 
 
@@ -346,7 +346,7 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
                 src.append(f"  cudaGetSymbolAddress((void**)&t.{fld}, {sym}{cid});")
             src.append(f"  t.nlo_lvl = {len(sc['lo_lvl']) - 1}; t.nb = {sc['nb']}; "
                        f"t.nup_lvl = {len(sc['up_lvl']) - 1}; t.ncombo = {len(sc['combo'])}; "
-                       f"t.nslots = {sc['nslots']};")
+                       f"t.nslots = {sc['nslots']}; t.tgt0 = {sc['tgt'][0]};")
             src.append(f"  launch_coop<CoopCls{cid}>(t, a);")
             src.append("}")
             if any(n == "coopw" for n, _ in vs):
@@ -357,7 +357,7 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
                     src.append(f"  cudaGetSymbolAddress((void**)&t.{fld}, {sym}{cid});")
                 src.append(f"  t.nlo_lvl = {len(sc['lo_lvl']) - 1}; t.nb = {sc['nb']}; "
                            f"t.nup_lvl = {len(sc['up_lvl']) - 1}; t.ncombo = {len(sc['combo'])}; "
-                           f"t.nslots = {sc['nslots']};")
+                           f"t.nslots = {sc['nslots']}; t.tgt0 = {sc['tgt'][0]};")
                 src.append(f"  launch_coopw<CoopCls{cid}>(t, a);")
                 src.append("}")
         for name, expr in vs:

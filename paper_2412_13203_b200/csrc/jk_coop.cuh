@@ -33,6 +33,7 @@ struct CoopTables {
   int ncombo;
   const unsigned short* tgt;
   int nslots;
+  int tgt0;  // outputs occupy slots [tgt0, tgt0 + NV) in kernel order (final copy level)
 };
 
 // C::BOYS_SMEM: stage the class's Boys slice in shared memory (51 KB) or read
@@ -368,7 +369,9 @@ template <class C>
 __global__ void __launch_bounds__(32 * kCoopWarps) coopw_kernel(CoopTables tb, LaunchArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int region = kCoopBase + kCoopMaxCombo + tb.nslots;
+  constexpr int DBLK = C::NA * C::NB + C::NC * C::ND + C::NA * C::NC + C::NB * C::ND + C::NA * C::ND +
+                       C::NB * C::NC;
+  const int region = kCoopBase + kCoopMaxCombo + tb.nslots + DBLK;
   double* coefb = smem + static_cast<size_t>(wid) * region;
   double* cf = coefb + kCoopBase;
   double* val = cf + kCoopMaxCombo;
@@ -420,49 +423,65 @@ __global__ void __launch_bounds__(32 * kCoopWarps) coopw_kernel(CoopTables tb, L
       coopw_eval<C>(tb, bm, km, a.prims, btab, coefb, cf, val, lane);
       const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (x != y ? 2.0 : 1.0);
       const double wj = 0.5 * deg, wk = 0.25 * deg;
+      // the six density blocks of this quartet, staged once per quartet:
+      // [Dcd | Dab | Dbd | Dac | Dbc | Dad] feed [J_ab | J_cd | K_ac | K_bd | K_ad | K_bc]
+      double* dsm = val + tb.nslots;
+      constexpr int E1 = NC * ND, E2 = E1 + NA * NB, E3 = E2 + NB * ND, E4 = E3 + NA * NC, E5 = E4 + NB * NC,
+                    E6 = E5 + NA * ND;
+      for (int o = lane; o < E6; o += 32) {
+        size_t r, cidx;
+        if (o < E1) { r = km.bfa + o / ND; cidx = km.bfb + o % ND; }                     // Dcd
+        else if (o < E2) { r = bm.bfa + (o - E1) / NB; cidx = bm.bfb + (o - E1) % NB; }  // Dab
+        else if (o < E3) { r = bm.bfb + (o - E2) / ND; cidx = km.bfb + (o - E2) % ND; }  // Dbd
+        else if (o < E4) { r = bm.bfa + (o - E3) / NC; cidx = km.bfa + (o - E3) % NC; }  // Dac
+        else if (o < E5) { r = bm.bfb + (o - E4) / NC; cidx = km.bfa + (o - E4) % NC; }  // Dbc
+        else { r = bm.bfa + (o - E5) / ND; cidx = km.bfb + (o - E5) % ND; }              // Dad
+        dsm[o] = __ldg(a.D + r * n + cidx);
+      }
+      __syncwarp();
+      const double* Dcd = dsm;             // NC x ND
+      const double* Dab = dsm + E1;        // NA x NB
+      const double* Dbd = dsm + E2;        // NB x ND
+      const double* Dac = dsm + E3;        // NA x NC
+      const double* Dbc = dsm + E4;        // NB x NC
+      const double* Dad = dsm + E5;        // NA x ND
       for (int o = lane; o < O6; o += 32) {
         double s = 0.0;
         double* dst;
         if (o < O1) {
           const int ia = o / NB, ib = o % NB;
           for (int ic = 0; ic < NC; ++ic)
-            for (int id = 0; id < ND; ++id)
-              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (km.bfa + ic) * n + km.bfb + id), s);
+            for (int id = 0; id < ND; ++id) s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], Dcd[ic * ND + id], s);
           dst = a.J + (bm.bfa + ia) * n + bm.bfb + ib;
           s *= wj;
         } else if (o < O2) {
           const int ic = (o - O1) / ND, id = (o - O1) % ND;
           for (int ia = 0; ia < NA; ++ia)
-            for (int ib = 0; ib < NB; ++ib)
-              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfa + ia) * n + bm.bfb + ib), s);
+            for (int ib = 0; ib < NB; ++ib) s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], Dab[ia * NB + ib], s);
           dst = a.J + (km.bfa + ic) * n + km.bfb + id;
           s *= wj;
         } else if (o < O3) {
           const int ia = (o - O2) / NC, ic = (o - O2) % NC;
           for (int ib = 0; ib < NB; ++ib)
-            for (int id = 0; id < ND; ++id)
-              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfb + ib) * n + km.bfb + id), s);
+            for (int id = 0; id < ND; ++id) s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], Dbd[ib * ND + id], s);
           dst = a.K + (bm.bfa + ia) * n + km.bfa + ic;
           s *= wk;
         } else if (o < O4) {
           const int ib = (o - O3) / ND, id = (o - O3) % ND;
           for (int ia = 0; ia < NA; ++ia)
-            for (int ic = 0; ic < NC; ++ic)
-              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfa + ia) * n + km.bfa + ic), s);
+            for (int ic = 0; ic < NC; ++ic) s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], Dac[ia * NC + ic], s);
           dst = a.K + (bm.bfb + ib) * n + km.bfb + id;
           s *= wk;
         } else if (o < O5) {
           const int ia = (o - O4) / ND, id = (o - O4) % ND;
           for (int ib = 0; ib < NB; ++ib)
-            for (int ic = 0; ic < NC; ++ic)
-              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfb + ib) * n + km.bfa + ic), s);
+            for (int ic = 0; ic < NC; ++ic) s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], Dbc[ib * NC + ic], s);
           dst = a.K + (bm.bfa + ia) * n + km.bfb + id;
           s *= wk;
         } else {
           const int ib = (o - O5) / NC, ic = (o - O5) % NC;
           for (int ia = 0; ia < NA; ++ia)
-            for (int id = 0; id < ND; ++id)
-              s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], __ldg(a.D + (bm.bfa + ia) * n + km.bfb + id), s);
+            for (int id = 0; id < ND; ++id) s = fma(val[__ldg(tb.tgt + ((ia * NB + ib) * NC + ic) * ND + id)], Dad[ia * ND + id], s);
           dst = a.K + (bm.bfb + ib) * n + km.bfa + ic;
           s *= wk;
         }
@@ -475,7 +494,9 @@ __global__ void __launch_bounds__(32 * kCoopWarps) coopw_kernel(CoopTables tb, L
 
 template <class C>
 void launch_coopw(const CoopTables& tb, const LaunchArgs& a) {
-  const size_t smem = sizeof(double) * kCoopWarps * (kCoopBase + kCoopMaxCombo + tb.nslots);
+  constexpr int DBLK = C::NA * C::NB + C::NC * C::ND + C::NA * C::NC + C::NB * C::ND + C::NA * C::ND +
+                       C::NB * C::NC;
+  const size_t smem = sizeof(double) * kCoopWarps * (kCoopBase + kCoopMaxCombo + tb.nslots + DBLK);
   const long long n = a.mode == 0 ? a.nitems : (a.mode == 1 ? a.npair_list : a.nq);
   if (n <= 0) return;
   static int blocks_per_sm = 0, sms = 0;
