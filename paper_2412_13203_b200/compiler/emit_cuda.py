@@ -267,6 +267,10 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append((f"lane_m{m}", f"launch_class<Cls{cid}, {m}, kLoopPrefetch>"))
         if info["ops"] > MINB_SMALL_OPS:
             out.append(("lane_plm2", f"launch_class<Cls{cid}, 2, kLoopPlain>"))
+        if info["ops"] > 100:
+            # up to 255 registers (1 CTA of 8 warps per SM): trades occupancy
+            # for the spills of the large-NV plans
+            out.append(("lane_plm1", f"launch_class<Cls{cid}, 1, kLoopPlain>"))
             out.append(("lane_sbm2", f"launch_class<Cls{cid}, 2, kLoopSmemBra>"))
         if info["ops"] <= MINB_SMALL_OPS:
             # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads

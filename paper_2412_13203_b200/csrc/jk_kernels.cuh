@@ -355,6 +355,8 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
     const int xkey = active ? x : -1;
     const int xnext = __shfl_down_sync(0xffffffffu, xkey, 1);
     const bool tail = active && (lane == 31 || xnext != xkey);
+    // common case: one bra for the whole warp -> plain butterfly sum
+    const bool one_bra = __all_sync(0xffffffffu, !active || x == it.bra0);
 #pragma unroll
     for (int a = 0; a < C::NA; ++a)
 #pragma unroll
@@ -365,8 +367,15 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
           for (int d = 0; d < C::ND; ++d)
             s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dcd + c2 * n + d), s);
-        s = seg_sum(s * wj, xkey, lane);
-        if (tail) red_add(J + (bm.bfa + a) * n + bm.bfb + b, s);
+        s *= wj;
+        if (one_bra) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == 0) red_add(J + (bm.bfa + a) * n + bm.bfb + b, s);
+        } else {
+          s = seg_sum(s, xkey, lane);
+          if (tail) red_add(J + (bm.bfa + a) * n + bm.bfb + b, s);
+        }
       }
     if (active) {
 #pragma unroll
