@@ -271,6 +271,7 @@ def variants(info) -> List[Tuple[str, str]]:
             # up to 255 registers (1 CTA of 8 warps per SM): trades occupancy
             # for the spills of the large-NV plans
             out.append(("lane_plm1", f"launch_class<Cls{cid}, 1, kLoopPlain>"))
+            out.append(("lane_pl384", f"launch_class<Cls{cid}, 1, kLoopPlain, 384>"))
             out.append(("lane_sbm2", f"launch_class<Cls{cid}, 2, kLoopSmemBra>"))
         if info["ops"] <= MINB_SMALL_OPS:
             # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads
@@ -294,6 +295,7 @@ def variants(info) -> List[Tuple[str, str]]:
         out.append(("fam_pl768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 768>"))
         out.append(("fam_x768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 768>"))
         out.append(("fam_x1024", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 1024>"))
+        out.append(("fam_x384", f"launch_fam<Cls{cid}, 1, kLoopPlain, 384, 768>"))
     assert len(out) <= 16, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 
