@@ -122,7 +122,7 @@ def emit_class(cls) -> Tuple[str, Dict]:
     b("const double T = rho * fma(PQx, PQx, fma(PQy, PQy, PQz * PQz));")
     b("const double pref = bp.U * kp.U * rs;")
     b(f"double F[{M + 1}];")
-    b(f"boys_eval<{M}>(T, btab, F);")
+    b("boys_eval_m1(T, btab, F);" if M == 1 else f"boys_eval<{M}>(T, btab, F);")
     if M > 0:
         b("const double WPx = -qinv * PQx, WPy = -qinv * PQy, WPz = -qinv * PQz;")
         b("const double WQx = pinv * PQx, WQy = pinv * PQy, WQz = pinv * PQz;")

@@ -67,7 +67,7 @@ __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const
 template <class C, int MB, int MK, int MINB, int STYLE, int NT>
 __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long long i0, long long i1) {
   extern __shared__ __align__(16) double s_boys[];
-  load_boys_slice(s_boys, a.boys_tab, C::M);
+  load_boys_for<C>(s_boys, a.boys_tab);
   const int lane = threadIdx.x & 31;
   const size_t n = static_cast<size_t>(a.N);
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 template <class C, int MB, int MK, int MINB, int STYLE, int NT>
 void launch_fam_seg(const LaunchArgs& a, long long i0, long long i1) {
   if (i1 <= i0) return;
-  const size_t smem = sizeof(double) * kBoysRows * kBoysCols;
+  const size_t smem = BoysStage<C>::bytes;
   static int blocks_per_sm = 0, sms = 0;
   if (!blocks_per_sm) {
     cudaFuncSetAttribute(jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,

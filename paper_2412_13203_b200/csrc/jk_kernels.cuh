@@ -125,6 +125,37 @@ __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ t
   }
 }
 
+// F_0, F_1 for M = 1 classes from the slices 0 and 1 staged back to back
+// (tab0 = slice 0): T < 40 each order by its own 8-term Taylor series about
+// T_i (no exp(-T) polynomial, no recursion); T >= 40 F_0 = sqrt(pi/T)/2 and
+// F_1 = F_0 / (2T), where the dropped e^-T / (2T) is < 3e-17 of F_1.
+__device__ __forceinline__ void boys_eval_m1(double T, const double* __restrict__ tab0, double* F) {
+  if (T < kBoysTmax) {
+    const double sh = fma(T, 16.0, kBoysK[6]);
+    const int i = __double2loint(sh);
+    const double md = fma(sh - kBoysK[6], 0.0625, -T);
+    const double m2 = md * md, m4 = m2 * m2;
+    const double2* r0 = reinterpret_cast<const double2*>(tab0 + i * kBoysCols);
+    const double2* r1 = reinterpret_cast<const double2*>(tab0 + (kBoysRows + i) * kBoysCols);
+    {
+      const double2 c01 = r0[0], c23 = r0[1], c45 = r0[2], c67 = r0[3];
+      const double q0 = fma(fma(c23.y, md, c23.x), m2, fma(c01.y, md, c01.x));
+      const double q1 = fma(fma(c67.y, md, c67.x), m2, fma(c45.y, md, c45.x));
+      F[0] = fma(q1, m4, q0);
+    }
+    {
+      const double2 c01 = r1[0], c23 = r1[1], c45 = r1[2], c67 = r1[3];
+      const double q0 = fma(fma(c23.y, md, c23.x), m2, fma(c01.y, md, c01.x));
+      const double q1 = fma(fma(c67.y, md, c67.x), m2, fma(c45.y, md, c45.x));
+      F[1] = fma(q1, m4, q0);
+    }
+  } else {
+    const double rt = rsqrt_pos(T);
+    F[0] = kBoysK[8] * rt;
+    F[1] = F[0] * (0.5 * rt * rt);
+  }
+}
+
 // Primitive loop nests over the class's prim()/finish() (compiler/
 // emit_cuda.py). Every style evaluates the same terms in the same order per
 // accumulator; they differ in how bra records are staged in registers:
@@ -265,6 +296,25 @@ __device__ __forceinline__ double seg_sum(double v, int key, int lane) {
   return v;
 }
 
+// Shared-memory Boys staging of a lane class: M = 1 classes stage slices 0
+// and 1 and evaluate both orders by their own Taylor series (boys_eval_m1);
+// every other class stages slice M.
+template <class C>
+struct BoysStage {
+  static constexpr int base = C::M == 1 ? 0 : C::M;
+  static constexpr int nsl = C::M == 1 ? 2 : 1;
+  static constexpr size_t bytes = sizeof(double) * kBoysRows * kBoysCols * nsl;
+};
+
+template <class C>
+__device__ __forceinline__ void load_boys_for(double* s_boys, const double* boys_tab) {
+  const double2* gt =
+      reinterpret_cast<const double2*>(boys_tab + static_cast<size_t>(BoysStage<C>::base) * kBoysRows * kBoysCols);
+  double2* st = reinterpret_cast<double2*>(s_boys);
+  for (int t = threadIdx.x; t < BoysStage<C>::nsl * kBoysRows * kBoysCols / 2; t += blockDim.x) st[t] = gt[t];
+  __syncthreads();
+}
+
 __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* boys_tab, int M) {
   const double2* gt = reinterpret_cast<const double2*>(boys_tab + static_cast<size_t>(M) * kBoysRows * kBoysCols);
   double2* st = reinterpret_cast<double2*>(s_boys);
@@ -283,10 +333,10 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
                                                        double* __restrict__ K, int N,
                                                        const double* __restrict__ boys_tab) {
   extern __shared__ __align__(16) double s_boys[];
-  load_boys_slice(s_boys, boys_tab, C::M);
+  load_boys_for<C>(s_boys, boys_tab);
 
   const int lane = threadIdx.x & 31;
-  PrimRec* sbra = reinterpret_cast<PrimRec*>(s_boys + kBoysRows * kBoysCols) + (threadIdx.x >> 5) * kSmemBraMax;
+  PrimRec* sbra = reinterpret_cast<PrimRec*>(s_boys + BoysStage<C>::nsl * kBoysRows * kBoysCols) + (threadIdx.x >> 5) * kSmemBraMax;
   int staged = -1;  // bra pair whose records sit in sbra (warp-uniform)
   (void)sbra;
   (void)staged;
@@ -453,7 +503,7 @@ __global__ void __launch_bounds__(128) schwarz_kernel(const int* __restrict__ li
                                                       double* __restrict__ Q,
                                                       const double* __restrict__ boys_tab) {
   extern __shared__ __align__(16) double s_boys[];
-  load_boys_slice(s_boys, boys_tab, C::M);
+  load_boys_for<C>(s_boys, boys_tab);
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int x = list[i];
@@ -483,7 +533,7 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
                                                       double* __restrict__ out,
                                                       const double* __restrict__ boys_tab) {
   extern __shared__ __align__(16) double s_boys[];
-  load_boys_slice(s_boys, boys_tab, C::M);
+  load_boys_for<C>(s_boys, boys_tab);
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const PairMeta b = pm[qp[2 * i]], k = pm[qp[2 * i + 1]];
@@ -501,7 +551,7 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 // leave the rest of the 256 KB L1/shared array to L1 (primitive records).
 template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
 void launch_class(const LaunchArgs& a) {
-  const size_t smem = sizeof(double) * kBoysRows * kBoysCols +
+  const size_t smem = BoysStage<C>::bytes +
                       (STYLE == kLoopSmemBra && a.mode == 0 ? sizeof(PrimRec) * kSmemBraMax * (NT / 32) : 0);
   if (a.mode == 0) {
     if (a.nitems <= 0) return;
