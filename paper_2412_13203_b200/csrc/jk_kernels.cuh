@@ -284,6 +284,10 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 #endif
 }
 
+__device__ __forceinline__ void prefetch_l1(const double* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // Inclusive segmented sum over lanes with equal non-decreasing key; lanes
 // whose key differs from lane+1 (segment tails) end holding the segment sum.
 __device__ __forceinline__ double seg_sum(double v, int key, int lane) {
@@ -341,9 +345,12 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
   (void)sbra;
   (void)staged;
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  for (long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       w < nitems; w += warps) {
-    const WorkItem it = items[w];
+  long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  WorkItem nxt = w < nitems ? items[w] : WorkItem{};
+  for (; w < nitems; w += warps) {
+    // the next task's descriptor is fetched one task ahead (hides its L2 trip)
+    const WorkItem it = nxt;
+    if (w + warps < nitems) nxt = items[w + warps];
     const int nq = it.r0nq >> 24;
     const bool active = lane < nq;
     // walk the per-bra survivor counts to this lane's (bra, ket)
