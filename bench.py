@@ -198,11 +198,19 @@ def cpu_sample(args, steps: int, warmup: int, target_s: float, reference_arm: bo
 # ------------------------------------------------------------------ GPU arm
 def run_ours(args, rank, nranks, local_rank):
     import torch
+    # ERITILE_DIST_BACKEND=gloo: test hook that runs N ranks on fewer GPUs
+    # (ranks share devices round-robin; NCCL needs one GPU per rank)
+    backend = os.environ.get("ERITILE_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dist = None
     if nranks > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     from paper_2412_13203_b200.eritile import Engine
 
     xyz, basis = workload(args)
