@@ -277,7 +277,6 @@ def variants(info) -> List[Tuple[str, str]]:
             # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads
             out.append(("lane_t512", f"launch_class<Cls{cid}, 1, kLoopPrefetch, 512>"))
             out.append(("lane_t768", f"launch_class<Cls{cid}, 1, kLoopPrefetch, 768>"))
-            out.append(("lane_pp512", f"launch_class<Cls{cid}, 1, kLoopPingPong, 512>"))
             out.append(("lane_pl512", f"launch_class<Cls{cid}, 1, kLoopPlain, 512>"))
             out.append(("lane_pl768", f"launch_class<Cls{cid}, 1, kLoopPlain, 768>"))
             out.append(("lane_sb512", f"launch_class<Cls{cid}, 1, kLoopSmemBra, 512>"))

@@ -328,7 +328,7 @@ __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* bo
 
 constexpr int kJkThreads = 256;
 
-template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
+template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads, int KR = 0>
 __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
                                                        const PairMeta* __restrict__ pm,
@@ -345,12 +345,20 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
   (void)sbra;
   (void)staged;
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  WorkItem nxt = w < nitems ? items[w] : WorkItem{};
-  for (; w < nitems; w += warps) {
-    // the next task's descriptor is fetched one task ahead (hides its L2 trip)
-    const WorkItem it = nxt;
-    if (w + warps < nitems) nxt = items[w + warps];
+  const size_t nK = static_cast<size_t>(N);
+  // KR: rows bfa.. (NA) and bfb.. (NB) of K for the chunk's leading bra are
+  // accumulated in shared memory (kbuf) and flushed once per chunk
+  double* kbuf = s_boys + BoysStage<C>::nsl * kBoysRows * kBoysCols;
+  int xcur = -1;
+  auto kadd_a = [&](int x, int a, size_t col, double v, int bfa) {
+    if (KR && x == xcur) atomicAdd(kbuf + static_cast<size_t>(a) * nK + col, v);
+    else red_add(K + (bfa + a) * nK + col, v);
+  };
+  auto kadd_b = [&](int x, int b, size_t col, double v, int bfb) {
+    if (KR && x == xcur) atomicAdd(kbuf + static_cast<size_t>(C::NA + b) * nK + col, v);
+    else red_add(K + (bfb + b) * nK + col, v);
+  };
+  auto process = [&](const WorkItem& it) {
     const int nq = it.r0nq >> 24;
     const bool active = lane < nq;
     // walk the per-bra survivor counts to this lane's (bra, ket)
@@ -458,7 +466,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbd + b * n + d), s);
-          red_add(K + (bm.bfa + a) * n + km.bfa + c2, s * wk);
+          kadd_a(x, a, km.bfa + c2, s * wk, bm.bfa);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int c2 = 0; c2 < C::NC; ++c2)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dac + a * n + c2), s);
-          red_add(K + (bm.bfb + b) * n + km.bfb + d, s * wk);
+          kadd_b(x, b, km.bfb + d, s * wk, bm.bfb);
         }
       // K_ad += sum_bc v D_bc ; K_bc += sum_ad v D_ad
 #pragma unroll
@@ -483,7 +491,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int c2 = 0; c2 < C::NC; ++c2)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbc + b * n + c2), s);
-          red_add(K + (bm.bfa + a) * n + km.bfb + d, s * wk);
+          kadd_a(x, a, km.bfb + d, s * wk, bm.bfa);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
@@ -495,8 +503,40 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dad + a * n + d), s);
-          red_add(K + (bm.bfb + b) * n + km.bfa + c2, s * wk);
+          kadd_b(x, b, km.bfa + c2, s * wk, bm.bfb);
         }
+    }
+  };
+  if constexpr (KR) {
+    constexpr int kRows = C::NA + C::NB;
+    constexpr long long kChunk = (NT / 32) * 8;  // items per CTA chunk
+    const long long nchunks = (nitems + kChunk - 1) / kChunk;
+    for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+      const long long w0 = ch * kChunk, w1 = (w0 + kChunk < nitems) ? w0 + kChunk : nitems;
+      xcur = items[w0].bra0;
+      const int bfa_cur = pm[xcur].bfa, bfb_cur = pm[xcur].bfb;
+      for (size_t e = threadIdx.x; e < kRows * nK; e += NT) kbuf[e] = 0.0;
+      __syncthreads();
+      for (long long w = w0 + (threadIdx.x >> 5); w < w1; w += NT / 32) process(items[w]);
+      __syncthreads();
+      for (size_t e = threadIdx.x; e < kRows * nK; e += NT) {
+        const double v = kbuf[e];
+        if (v != 0.0) {
+          const int r = static_cast<int>(e / nK);
+          const size_t col = e % nK;
+          red_add(K + (r < C::NA ? bfa_cur + r : bfb_cur + (r - C::NA)) * nK + col, v);
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    WorkItem nxt = w < nitems ? items[w] : WorkItem{};
+    for (; w < nitems; w += warps) {
+      // the next task's descriptor is fetched one task ahead (hides its L2 trip)
+      const WorkItem it = nxt;
+      if (w + warps < nitems) nxt = items[w + warps];
+      process(it);
     }
   }
 }
@@ -556,8 +596,33 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 // NT: threads per CTA. One Boys slice is staged per CTA, so 512/768-thread
 // CTAs at MINB = 1 keep 16/24 warps per SM with a single 51 KB table and
 // leave the rest of the 256 KB L1/shared array to L1 (primitive records).
-template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
+// KR = 1: K rows of each chunk's leading bra accumulated in shared memory
+// ((NA + NB) x N doubles); when they do not fit, the KR = 0 kernel runs.
+// Measured 3-30% slower than the RED.ADD.F64 path on (H2O)_80 (shared FP64
+// atomics are CAS loops on sm_100a), so no registry variant uses it; kept
+// as the allocator's hook for systems with heavier K-row reuse.
+template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads, int KR = 0>
 void launch_class(const LaunchArgs& a) {
+  if constexpr (KR) {
+    if (a.mode != 0) return launch_class<C, MINB, STYLE, NT, 0>(a);
+    if (a.nitems <= 0) return;
+    const size_t smem = BoysStage<C>::bytes + sizeof(double) * (C::NA + C::NB) * static_cast<size_t>(a.N);
+    if (smem > 220 * 1024) return launch_class<C, MINB, STYLE, NT, 0>(a);
+    cudaFuncSetAttribute(jk_kernel<C, MINB, STYLE, NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    int bps = 0, sms = 0, dev = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, jk_kernel<C, MINB, STYLE, NT, 1>, NT, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (bps < 1) return launch_class<C, MINB, STYLE, NT, 0>(a);
+    const long long chunk = (NT / 32) * 8;
+    const long long want = (a.nitems + chunk - 1) / chunk;
+    const long long cap = static_cast<long long>(bps) * sms;
+    const int grid = static_cast<int>(want < cap ? want : cap);
+    jk_kernel<C, MINB, STYLE, NT, 1><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D,
+                                                                  a.J, a.K, a.N, a.boys_tab);
+    return;
+  }
   const size_t smem = BoysStage<C>::bytes +
                       (STYLE == kLoopSmemBra && a.mode == 0 ? sizeof(PrimRec) * kSmemBraMax * (NT / 32) : 0);
   if (a.mode == 0) {
