@@ -294,3 +294,15 @@ def test_edge_cases_empty_and_tiny(gpu):
         Jo, Ko, nq = O.build_jk(D, 0.0)
         assert nq == e.num_quartets()
         assert np.max(np.abs(J - Jo)) < 1e-12 and np.max(np.abs(K - Ko)) < 1e-12
+
+
+def test_concurrent_and_serial_launches_agree(gpu):
+    """Class launches on 4 streams (default) and on one stream give the same
+    J/K up to FP64 atomic summation order."""
+    xyz, bas = geom("w4"), BASIS["cc-pvdz"]
+    e = _engine(xyz, bas, 1e-10)
+    D = _rand_density(e.nbf, 21)
+    J1, K1 = e.build_jk(D)
+    e.set_concurrent(False)
+    J2, K2 = e.build_jk(D)
+    assert np.max(np.abs(J1 - J2)) < 1e-12 and np.max(np.abs(K1 - K2)) < 1e-12
