@@ -306,3 +306,28 @@ def test_concurrent_and_serial_launches_agree(gpu):
     e.set_concurrent(False)
     J2, K2 = e.build_jk(D)
     assert np.max(np.abs(J1 - J2)) < 1e-12 and np.max(np.abs(K1 - K2)) < 1e-12
+
+
+def test_ss_closed_form_and_bra_ket_symmetry(gpu):
+    """(ss|ss) of unit-exponent Gaussians is pi^(5/2)/4 before
+    normalisation, i.e. 2/sqrt(pi) for normalised functions; and the
+    bra<->ket permutation identity on 200 random quartets (all L<=2 classes
+    of benzene/6-31G*)."""
+    import math
+    from paper_2412_13203_b200.eritile import Engine
+    basis = "element H\n0 1\n1.0 1.0\n"
+    e = Engine(0).load_molecule("1\nunit s\nH 0 0 0\n", basis).build_pairs(0.0)
+    v = e.eri_quartet(0, 0)
+    assert abs(v[0] - 2.0 / math.sqrt(math.pi)) < 1e-14
+    assert abs(v[0] * (math.pi / 2.0) ** 3 - math.pi ** 2.5 / 4.0) < 1e-13
+    xyz, bas = geom("benzene"), BASIS["6-31g*"]
+    e = _engine(xyz, bas, 0.0)
+    L, _, _ = e.shell_info()
+    i, j = e.pair_shells()
+    nc = lambda l: (l + 1) * (l + 2) // 2
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        x, y = (int(t) for t in rng.integers(0, e.npairs, 2))
+        a = e.eri_quartet(x, y).reshape(nc(L[i[x]]) * nc(L[j[x]]), nc(L[i[y]]) * nc(L[j[y]]))
+        b = e.eri_quartet(y, x).reshape(nc(L[i[y]]) * nc(L[j[y]]), nc(L[i[x]]) * nc(L[j[x]]))
+        assert np.allclose(a, b.T, rtol=1e-12, atol=1e-14), (x, y)
