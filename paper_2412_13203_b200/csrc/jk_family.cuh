@@ -47,6 +47,12 @@ __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const
         if constexpr (MB == 2) C::prim_w(bq, kp, btab, wq.x, wq.y, s[0], s[MB - 1]);
         else C::prim_w1(bq, kp, btab, wq.x, s[0]);
       }
+    } else if constexpr (STYLE == kLoopSmemBra) {  // bra records / weights may sit in shared memory
+      for (int i = 0; i < kb; ++i) {
+        const double2 wq = bw[i];
+        if constexpr (MB == 2) C::prim_w(load_prim_gen<C::BPA>(bra + i), kp, btab, wq.x, wq.y, s[0], s[MB - 1]);
+        else C::prim_w1(load_prim_gen<C::BPA>(bra + i), kp, btab, wq.x, s[0]);
+      }
     } else {
       for (int i = 0; i < kb; ++i) {
         const double2 wq = __ldg(bw + i);
@@ -69,6 +75,16 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
   extern __shared__ __align__(16) double s_boys[];
   load_boys_for<C>(s_boys, a.boys_tab);
   const int lane = threadIdx.x & 31;
+  PrimRec* sbra = reinterpret_cast<PrimRec*>(s_boys + BoysStage<C>::nsl * kBoysRows * kBoysCols) +
+                  (threadIdx.x >> 5) * kSmemBraMax;
+  double2* sbw = reinterpret_cast<double2*>(reinterpret_cast<PrimRec*>(s_boys + BoysStage<C>::nsl * kBoysRows *
+                                                                                    kBoysCols) +
+                                            (NT / 32) * kSmemBraMax) +
+                 (threadIdx.x >> 5) * kSmemBraMax;
+  int staged = -1;
+  (void)sbra;
+  (void)sbw;
+  (void)staged;
   const size_t n = static_cast<size_t>(a.N);
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   for (long long w = i0 + static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < i1;
@@ -87,8 +103,26 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
     const UnitMeta bu = a.um[x];
     const UnitMeta ku = a.um[y];
     typename C::Acc acc[MB][MK];
-    fam_drive<C, MB, MK, STYLE>(a.prims + bu.prim_off, a.uw + bu.prim_off, bu.K, a.prims + ku.prim_off,
-                        a.uw + ku.prim_off, active ? ku.K : 0, s_boys, acc);
+    const PrimRec* brap = a.prims + bu.prim_off;
+    const double2* bwp = a.uw + bu.prim_off;
+    if constexpr (STYLE == kLoopSmemBra) {  // stage the warp's bra unit once while it stays
+      const int x0 = __shfl_sync(0xffffffffu, x, 0);
+      if (__all_sync(0xffffffffu, x == x0) && bu.K <= kSmemBraMax) {
+        if (x0 != staged) {
+          __syncwarp();
+          const double2* src = reinterpret_cast<const double2*>(a.prims + bu.prim_off);
+          double2* dst = reinterpret_cast<double2*>(sbra);
+          for (int t = lane; t < bu.K * 5; t += 32) dst[t] = __ldg(src + t);
+          for (int t = lane; t < bu.K; t += 32) sbw[t] = __ldg(a.uw + bu.prim_off + t);
+          __syncwarp();
+          staged = x0;
+        }
+        brap = sbra;
+        bwp = sbw;
+      }
+    }
+    fam_drive<C, MB, MK, STYLE>(brap, bwp, bu.K, a.prims + ku.prim_off, a.uw + ku.prim_off, active ? ku.K : 0,
+                                s_boys, acc);
     constexpr int nmb = MB, nmk = MK;
     const int xkey = active ? x : -1;
     const int xnext = __shfl_down_sync(0xffffffffu, xkey, 1);
@@ -211,7 +245,8 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 template <class C, int MB, int MK, int MINB, int STYLE, int NT>
 void launch_fam_seg(const LaunchArgs& a, long long i0, long long i1) {
   if (i1 <= i0) return;
-  const size_t smem = BoysStage<C>::bytes;
+  const size_t smem =
+      BoysStage<C>::bytes + (STYLE == kLoopSmemBra ? (sizeof(PrimRec) + sizeof(double2)) * kSmemBraMax * (NT / 32) : 0);
   static int blocks_per_sm = 0, sms = 0;
   if (!blocks_per_sm) {
     cudaFuncSetAttribute(jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
