@@ -122,7 +122,7 @@ def emit_class(cls) -> Tuple[str, Dict]:
     b("const double T = rho * fma(PQx, PQx, fma(PQy, PQy, PQz * PQz));")
     b("const double pref = bp.U * kp.U * rs;")
     b(f"double F[{M + 1}];")
-    b("boys_eval_m1(T, btab, F);" if M == 1 else f"boys_eval<{M}>(T, btab, F);")
+    b("boys_eval_m1(T, btab, F);" if (M == 1 and BOYS_M1_TWO_SLICES) else f"boys_eval<{M}>(T, btab, F);")
     if M > 0:
         b("const double WPx = -qinv * PQx, WPy = -qinv * PQy, WPz = -qinv * PQz;")
         b("const double WQx = pinv * PQx, WQy = pinv * PQy, WQz = pinv * PQz;")
@@ -161,6 +161,7 @@ def emit_class(cls) -> Tuple[str, Dict]:
     w(f"  static constexpr int NV = {na * nb * nc * nd};")
     w(f"  static constexpr int M = {M};")
     w(f"  static constexpr int OPS = {plan.op_count};")
+    w(f"  static constexpr bool BOYS_M1_TWO = {'true' if (M == 1 and BOYS_M1_TWO_SLICES) else 'false'};")
     w(f"  static constexpr bool BPA = {'true' if 'bPA' in optext else 'false'};  // plan reads bra PA")
     w(f"  static constexpr bool KPA = {'true' if 'kPA' in optext else 'false'};  // plan reads ket PA (QC)")
     w("  struct Acc { double " + ", ".join(bnd_name[n] for n in plan.boundary) + "; };")
@@ -254,6 +255,9 @@ MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2, 3)
 COOP_SMEM_BUDGET = 110 * 1024
 COOPW_MAX_SLOTS = 5500  # 4 warps x (slots + 112) doubles <= ~196 KB
+# M = 1 classes evaluating F_0 and F_1 from two staged table slices: measured
+# neutral-to-slower (the second 51 KB slice costs L1 capacity), off
+BOYS_M1_TWO_SLICES = False
 FAM_MAX_BOUNDARY = int(os.environ.get("ERITILE_FAM_MAX_BOUNDARY", "9"))  # keep >= 2 CTAs/SM when the Boys slice is staged
 
 
@@ -333,7 +337,8 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
             src.append(f"struct Cls{cid} {{\n  static constexpr int LA = {cls[0]}, LB = {cls[1]}, "
                        f"LC = {cls[2]}, LD = {cls[3]};\n  static constexpr int NA = {na}, NB = {nb}, "
                        f"NC = {nc}, ND = {nd};\n  static constexpr int NV = {na * nb * nc * nd};\n"
-                       f"  static constexpr int M = {info['M']};\n  static constexpr int OPS = {info['ops']};\n}};")
+                       f"  static constexpr int M = {info['M']};\n  static constexpr int OPS = {info['ops']};\n"
+                       f"  static constexpr bool BOYS_M1_TWO = false;\n}};")
         if coop:
             width = max(b - a for a, b in zip(sc["lo_lvl"], sc["lo_lvl"][1:]))
             nt = 256 if width >= 192 else 128

@@ -305,8 +305,9 @@ __device__ __forceinline__ double seg_sum(double v, int key, int lane) {
 // every other class stages slice M.
 template <class C>
 struct BoysStage {
-  static constexpr int base = C::M == 1 ? 0 : C::M;
-  static constexpr int nsl = C::M == 1 ? 2 : 1;
+  static constexpr bool two = C::M == 1 && C::BOYS_M1_TWO;
+  static constexpr int base = two ? 0 : C::M;
+  static constexpr int nsl = two ? 2 : 1;
   static constexpr size_t bytes = sizeof(double) * kBoysRows * kBoysCols * nsl;
 };
 
