@@ -257,6 +257,7 @@ void launch_fam_seg(const LaunchArgs& a, long long i0, long long i1) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
+    set_min_carveout(reinterpret_cast<const void*>(jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>), blocks_per_sm, smem);
   }
   const long long want = (i1 - i0 + (NT / 32) - 1) / (NT / 32);
   const long long cap = static_cast<long long>(blocks_per_sm) * sms;

@@ -329,6 +329,15 @@ __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* bo
 
 constexpr int kJkThreads = 256;
 
+// Shared-memory carveout just large enough for the resident CTAs, so the
+// rest of the SM's 256 KB L1/shared array caches primitive records.
+inline void set_min_carveout(const void* fn, int blocks_per_sm, size_t smem) {
+  const size_t need = static_cast<size_t>(blocks_per_sm) * (smem + 1024);
+  int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+  pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads, int KR = 0>
 __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
@@ -637,6 +646,7 @@ void launch_class(const LaunchArgs& a) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (blocks_per_sm < 1) blocks_per_sm = 1;
+      set_min_carveout(reinterpret_cast<const void*>(jk_kernel<C, MINB, STYLE, NT>), blocks_per_sm, smem);
     }
     const long long want = (a.nitems + (NT / 32) - 1) / (NT / 32);
     const long long cap = static_cast<long long>(blocks_per_sm) * sms;
