@@ -280,13 +280,11 @@ def variants(info) -> List[Tuple[str, str]]:
         if info["ops"] <= MINB_SMALL_OPS:
             # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads
             out.append(("lane_t512", f"launch_class<Cls{cid}, 1, kLoopPrefetch, 512>"))
-            out.append(("lane_t768", f"launch_class<Cls{cid}, 1, kLoopPrefetch, 768>"))
             out.append(("lane_pl512", f"launch_class<Cls{cid}, 1, kLoopPlain, 512>"))
             out.append(("lane_pl768", f"launch_class<Cls{cid}, 1, kLoopPlain, 768>"))
             out.append(("lane_sb512", f"launch_class<Cls{cid}, 1, kLoopSmemBra, 512>"))
         if info["ops"] <= UNROLL2_MAX_OPS:
             out.append(("lane_u2t512", f"launch_class<Cls{cid}, 1, kLoopTwoKet, 512>"))
-            out.append(("lane_pl1024", f"launch_class<Cls{cid}, 1, kLoopPlain, 1024>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
         if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:
@@ -297,8 +295,6 @@ def variants(info) -> List[Tuple[str, str]]:
         out.append(("fam_pl512", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512>"))
         out.append(("fam_pl768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 768>"))
         out.append(("fam_x768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 768>"))
-        out.append(("fam_x1024", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 1024>"))
-        out.append(("fam_x384", f"launch_fam<Cls{cid}, 1, kLoopPlain, 384, 768>"))
     assert len(out) <= 16, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 

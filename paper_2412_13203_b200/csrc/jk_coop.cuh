@@ -280,7 +280,8 @@ constexpr int kCoopWarps = 4;
 template <class C>
 __device__ __forceinline__ void coopw_eval(const CoopTables& tb, const PairMeta& bm, const PairMeta& km,
                                            const PrimRec* __restrict__ prims, const double* __restrict__ btab,
-                                           double* coefb, double* cf, double* val, int lane) {
+                                           const double* __restrict__ btab0, double* coefb, double* cf,
+                                           double* val, int lane) {
   for (int s = lane; s < tb.nb; s += 32) val[1 + s] = 0.0;
   const PrimRec* bra = prims + bm.prim_off;
   const PrimRec* ket = prims + km.prim_off;
@@ -312,6 +313,23 @@ __device__ __forceinline__ void coopw_eval(const CoopTables& tb, const PairMeta&
         coefb[kB_ITQ] = kp.i2p * pinv;
         coefb[kB_AB] = bm.ABx; coefb[kB_AB + 1] = bm.ABy; coefb[kB_AB + 2] = bm.ABz;
         coefb[kB_CD] = km.ABx; coefb[kB_CD + 1] = km.ABy; coefb[kB_CD + 2] = km.ABz;
+      }
+      if (T < kBoysTmax) {
+        // warp-uniform (one primitive quartet per warp): lane 2 + m evaluates
+        // F_m by its own 8-term Taylor series from table slice m (global,
+        // L1-resident), so the M+1 orders are computed in parallel
+        const int m = lane - 2;
+        if (m >= 0 && m <= C::M) {
+          const double sh = fma(T, 16.0, kBoysK[6]);
+          const int i = __double2loint(sh);
+          const double md = fma(sh - kBoysK[6], 0.0625, -T);
+          const double m2 = md * md;
+          const double2* r = reinterpret_cast<const double2*>(btab0 + (static_cast<size_t>(m) * kBoysRows + i) * kBoysCols);
+          const double2 c01 = __ldg(r), c23 = __ldg(r + 1), c45 = __ldg(r + 2), c67 = __ldg(r + 3);
+          const double q0 = fma(fma(c23.y, md, c23.x), m2, fma(c01.y, md, c01.x));
+          const double q1 = fma(fma(c67.y, md, c67.x), m2, fma(c45.y, md, c45.x));
+          coefb[kB_PF + m] = pref * fma(q1, m2 * m2, q0);
+        }
       } else if (lane == 2) {
         double F[C::M + 1];
         boys_eval<C::M>(T, btab, F);
@@ -390,7 +408,7 @@ __global__ void __launch_bounds__(32 * kCoopWarps) coopw_kernel(CoopTables tb, L
       const int xb = a.mode == 1 ? a.pair_list[i] : a.qpairs[2 * i];
       const int xk = a.mode == 1 ? xb : a.qpairs[2 * i + 1];
       const PairMeta bm = a.pm[xb], km = a.pm[xk];
-      coopw_eval<C>(tb, bm, km, a.prims, btab, coefb, cf, val, lane);
+      coopw_eval<C>(tb, bm, km, a.prims, btab, a.boys_tab, coefb, cf, val, lane);
       if (a.mode == 2) {
         for (int k = lane; k < C::NV; k += 32) a.qout[i * C::NV + k] = val[__ldg(tb.tgt + k)];
       } else {
@@ -420,7 +438,7 @@ __global__ void __launch_bounds__(32 * kCoopWarps) coopw_kernel(CoopTables tb, L
       }
       const int y = it.yfirst + q;
       const PairMeta bm = a.pm[x], km = a.pm[y];
-      coopw_eval<C>(tb, bm, km, a.prims, btab, coefb, cf, val, lane);
+      coopw_eval<C>(tb, bm, km, a.prims, btab, a.boys_tab, coefb, cf, val, lane);
       const double deg = (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (x != y ? 2.0 : 1.0);
       const double wj = 0.5 * deg, wk = 0.25 * deg;
       // the six density blocks of this quartet, staged once per quartet:
