@@ -163,12 +163,10 @@ __device__ __forceinline__ void boys_eval_m1(double T, const double* __restrict_
 //  kLoopPrefetch  next bra record loaded one step ahead (register rotation);
 //  kLoopTwoKet    two ket primitives per step share one bra record; two
 //                 accumulator sets, folded at the end;
-//  kLoopPingPong  bra loop unrolled by two with two record buffers, each
-//                 reloaded right after use (no register rotation copies).
 //  kLoopSmemBra   plain loop; when all lanes of the warp share the bra, its
 //                 primitive records are staged once in shared memory (per
 //                 warp, reused while consecutive items keep the bra).
-constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopTwoKet = 2, kLoopPingPong = 3, kLoopSmemBra = 4;
+constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopTwoKet = 2, kLoopSmemBra = 4;
 constexpr int kSmemBraMax = 81;  // records per warp buffer (cc-pVDZ s9 x s9)
 
 // Generic-address record load (the pointer may be shared or global).
@@ -233,18 +231,6 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
       for (int i = 0; i < kb; ++i) C::prim(load_prim<C::BPA>(bra + i), kp, btab, a);
     }
     C::fold(a, b);
-  } else {
-    for (int j = 0; j < kk; ++j) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j);
-      PrimRec b0 = load_prim<C::BPA>(bra);
-      PrimRec b1 = load_prim<C::BPA>(bra + (kb > 1 ? 1 : 0));
-      for (int i = 0; i < kb; i += 2) {
-        C::prim(b0, kp, btab, a);
-        b0 = load_prim<C::BPA>(bra + (i + 2 < kb ? i + 2 : kb - 1));
-        if (i + 1 < kb) C::prim(b1, kp, btab, a);
-        b1 = load_prim<C::BPA>(bra + (i + 3 < kb ? i + 3 : kb - 1));
-      }
-    }
   }
   C::finish(a, ABx, ABy, ABz, CDx, CDy, CDz, out);
 }
@@ -282,10 +268,6 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 #else
   atomicAdd(p, v);
 #endif
-}
-
-__device__ __forceinline__ void prefetch_l1(const double* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
 // Inclusive segmented sum over lanes with equal non-decreasing key; lanes
