@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -808,6 +809,15 @@ struct eritile_gpu {
       }
       cw.n = static_cast<long long>(items.size()) - cw.off;
       while (cur_seg < 4) cw.seg[++cur_seg] = cw.n;
+      if (std::getenv("ERITILE_DEBUG_ITEMS") && cw.n > 0) {  // diagnostics: items spanning > 1 bra
+        long long multi = 0;
+        for (long long w = cw.off; w < cw.off + cw.n; ++w) {
+          const WorkItem& it = items[w];
+          if ((it.r0nq & 0xffffff) + (it.r0nq >> 24) > cnt[it.cntp]) ++multi;
+        }
+        std::fprintf(stderr, "class %d fam %d items %lld multi-bra %.3f\n", cls, fam ? 1 : 0, cw.n,
+                     static_cast<double>(multi) / cw.n);
+      }
       if (cw.n > 0) {
         const ClassEntry& ce = kClassTable[cls];
         const double nv = static_cast<double>((ce.la + 1) * (ce.la + 2) / 2 * (ce.lb + 1) * (ce.lb + 2) / 2 *
