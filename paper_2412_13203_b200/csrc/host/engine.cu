@@ -611,7 +611,21 @@ struct eritile_gpu {
     }
     pm.swap(npm);
     Q.swap(nQ);
-    if (!host_only) d_pm.upload(pm);
+    // primitive records follow the new pair order: the kets of a warp (Q-
+    // consecutive pairs) then read one contiguous block of records, so L2
+    // lines and DRAM pages are used whole
+    std::vector<PrimRec> nprims;
+    nprims.reserve(prims.size());
+    for (PairMeta& m : pm) {
+      const int off = static_cast<int>(nprims.size());
+      nprims.insert(nprims.end(), prims.begin() + m.prim_off, prims.begin() + m.prim_off + m.K);
+      m.prim_off = off;
+    }
+    prims.swap(nprims);
+    if (!host_only) {
+      d_pm.upload(pm);
+      d_prims.upload(prims);
+    }
   }
 
   // Units of <= kFamMax product pairs with identical primitive records up to
