@@ -234,7 +234,7 @@ def emit_class(cls) -> Tuple[str, Dict]:
     w("      const PrimRec* __restrict__ bra, int kb, const PrimRec* __restrict__ ket, int kk,")
     w("      double ABx, double ABy, double ABz, double CDx, double CDy, double CDz,")
     w("      const double* __restrict__ btab, double (&out)[NV]) {")
-    w(f"    eri_drive<Cls{cid}, kLoopPrefetch>(bra, kb, ket, kk, ABx, ABy, ABz, CDx, CDy, CDz, btab, out);")
+    w(f"    eri_drive<Cls{cid}, kLoopPrefetch>(bra, kb, ket, kk, 1, ABx, ABy, ABz, CDx, CDy, CDz, btab, out);")
     w("  }")
     w("};")
     info = dict(cls=cls, swap=swap, ops=plan.op_count, M=M, nv=na * nb * nc * nd,

@@ -207,6 +207,7 @@ struct eritile_gpu {
   // product pairs
   std::vector<PairMeta> pm;   // product order
   std::vector<PrimRec> prims;
+  std::vector<PrimRec> kprims;  // group-transposed ket copy (build_ket_soa)
   std::vector<int> prod_of_ref;  // ref index -> product id
   std::vector<int> cls_of_pair;  // canonical pair class index per product pair
   std::vector<Group> groups;
@@ -224,7 +225,7 @@ struct eritile_gpu {
   int launches_last = 0;
 
   DevBuf<PairMeta> d_pm;
-  DevBuf<PrimRec> d_prims;
+  DevBuf<PrimRec> d_prims, d_kprims;
   DevBuf<double> d_boys, d_scale, d_Q;
   DevBuf<WorkItem> d_items;
   DevBuf<int> d_cnt;
@@ -363,6 +364,7 @@ struct eritile_gpu {
     a.cnt = d_cnt.p;
     a.pm = d_pm.p;
     a.prims = d_prims.p;
+    a.kprims = d_kprims.p;
     a.D = dDs;
     a.J = dJK;
     a.K = dJK + NN;
@@ -628,6 +630,27 @@ struct eritile_gpu {
     }
   }
 
+  // Group-transposed copy of the primitive records for ket reads: record j of
+  // the pair at rank p of group g sits at base_g + j * count_g + p, so the 32
+  // consecutive kets of a warp read 32 consecutive records (coalesced).
+  void build_ket_soa() {
+    kprims.assign(prims.size(), PrimRec{});
+    size_t base = 0;
+    for (const Group& g : groups) {
+      for (int p = 0; p < g.count; ++p) {
+        PairMeta& m = pm[g.first + p];
+        m.ksoa = static_cast<int>(base) + p;
+        m.kstride = g.count;
+        for (int j = 0; j < g.K; ++j) kprims[base + static_cast<size_t>(j) * g.count + p] = prims[m.prim_off + j];
+      }
+      base += static_cast<size_t>(g.K) * g.count;
+    }
+    if (!host_only) {
+      d_pm.upload(pm);
+      d_kprims.upload(kprims);
+    }
+  }
+
   // Units of <= kFamMax product pairs with identical primitive records up to
   // U: same oriented sibling shells and the same kept primitive index set,
   // taken in Q-descending order inside each product group. Unit groups are
@@ -716,6 +739,7 @@ struct eritile_gpu {
     if (t > 0.0 && !have_q) schwarz();
     tau = t;
     if (t > 0.0) sort_groups_by_q();
+    build_ket_soa();
     bool any_fam = false;
     for (int c = 0; c < kNumClasses; ++c) any_fam = any_fam || fam_active(c);
     if (any_fam) build_units();

@@ -22,8 +22,9 @@ struct alignas(16) PrimRec {
 // index (block.hpp:94-101) used to export quartet lists.
 struct alignas(16) PairMeta {
   int prim_off, K, bfa, bfb;
-  int sha, shb, ref, pad;
-  double ABx, ABy, ABz, pad2;
+  int sha, shb, ref, kstride;  // kstride: ket-record stride in kprims (group size)
+  double ABx, ABy, ABz;
+  int ksoa, pad;               // this pair's first ket record in kprims
 };
 
 // A warp task: 32 consecutive quartets of the flat survivor sequence of one
@@ -62,6 +63,7 @@ struct LaunchArgs {
   double* qout;          // mode 2: NV raw values per quartet, kernel order
   const PairMeta* pm;
   const PrimRec* prims;
+  const PrimRec* kprims;  // group-transposed copy of prims (ket reads of the lane kernels)
   const double* D;
   double* J;
   double* K;

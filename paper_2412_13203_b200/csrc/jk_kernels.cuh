@@ -188,24 +188,24 @@ __device__ __forceinline__ PrimRec load_prim_gen(const PrimRec* p) {
 
 template <class C, int STYLE>
 __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int kb,
-                                          const PrimRec* __restrict__ ket, int kk, double ABx, double ABy,
+                                          const PrimRec* __restrict__ ket, int kk, int ks, double ABx, double ABy,
                                           double ABz, double CDx, double CDy, double CDz,
                                           const double* __restrict__ btab, double (&out)[C::NV]) {
   typename C::Acc a;
   C::zero(a);
   if constexpr (STYLE == kLoopPlain) {
     for (int j = 0; j < kk; ++j) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
       for (int i = 0; i < kb; ++i) C::prim(load_prim<C::BPA>(bra + i), kp, btab, a);
     }
   } else if constexpr (STYLE == kLoopSmemBra) {
     for (int j = 0; j < kk; ++j) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
       for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
     }
   } else if constexpr (STYLE == kLoopPrefetch) {
     for (int j = 0; j < kk; ++j) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
       PrimRec bn = load_prim<C::BPA>(bra);
       for (int i = 0; i < kb; ++i) {
         const PrimRec bq = bn;
@@ -218,8 +218,8 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
     C::zero(b);
     int j = 0;
     for (; j + 1 < kk; j += 2) {
-      const PrimRec k0 = load_prim<C::KPA>(ket + j);
-      const PrimRec k1 = load_prim<C::KPA>(ket + j + 1);
+      const PrimRec k0 = load_prim<C::KPA>(ket + j * ks);
+      const PrimRec k1 = load_prim<C::KPA>(ket + (j + 1) * ks);
       for (int i = 0; i < kb; ++i) {
         const PrimRec bq = load_prim<C::BPA>(bra + i);
         C::prim(bq, k0, btab, a);
@@ -227,7 +227,7 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
       }
     }
     if (j < kk) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j);
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
       for (int i = 0; i < kb; ++i) C::prim(load_prim<C::BPA>(bra + i), kp, btab, a);
     }
     C::fold(a, b);
@@ -327,7 +327,8 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
                                                        const PrimRec* __restrict__ prims,
                                                        const double* __restrict__ D, double* __restrict__ J,
                                                        double* __restrict__ K, int N,
-                                                       const double* __restrict__ boys_tab) {
+                                                       const double* __restrict__ boys_tab,
+                                                       const PrimRec* __restrict__ kprims) {
   extern __shared__ __align__(16) double s_boys[];
   load_boys_for<C>(s_boys, boys_tab);
 
@@ -393,7 +394,12 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
           brap = sbra;
         }
       }
-      eri_drive<C, STYLE>(brap, bh.y, prims + kh.x, active ? kh.y : 0, ABx, ABy, ABz, CDx, CDy, CDz, s_boys, v);
+      // kets read from the group-transposed copy: record j of the warp's 32
+      // consecutive kets are 32 consecutive records (coalesced)
+      const int2 ks = __ldg(reinterpret_cast<const int2*>(&pm[y].ksoa));
+      const int kstride = __ldg(&pm[y].kstride);
+      eri_drive<C, STYLE>(brap, bh.y, kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy, CDz,
+                          s_boys, v);
     }
     PairMeta bm, km;
     ld_meta_late(pm + x, bm);
@@ -612,7 +618,7 @@ void launch_class(const LaunchArgs& a) {
     const long long cap = static_cast<long long>(bps) * sms;
     const int grid = static_cast<int>(want < cap ? want : cap);
     jk_kernel<C, MINB, STYLE, NT, 1><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D,
-                                                                  a.J, a.K, a.N, a.boys_tab);
+                                                                  a.J, a.K, a.N, a.boys_tab, a.kprims);
     return;
   }
   const size_t smem = BoysStage<C>::bytes +
@@ -634,7 +640,7 @@ void launch_class(const LaunchArgs& a) {
     const long long cap = static_cast<long long>(blocks_per_sm) * sms;
     const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
     jk_kernel<C, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
-                                                       a.K, a.N, a.boys_tab);
+                                                       a.K, a.N, a.boys_tab, a.kprims);
   } else if (a.mode == 2) {
     if (a.nq <= 0) return;
     cudaFuncSetAttribute(quartet_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
