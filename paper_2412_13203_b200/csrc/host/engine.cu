@@ -241,8 +241,11 @@ struct eritile_gpu {
   std::vector<Group> ugroups;
   std::vector<double> uQ;
   std::vector<double2> uw;
+  std::vector<PrimRec> ukprims;
+  std::vector<double2> ukw;
   DevBuf<UnitMeta> d_um;
-  DevBuf<double2> d_uw;
+  DevBuf<double2> d_uw, d_ukw;
+  DevBuf<PrimRec> d_ukprims;
   DevBuf<double> d_Qp;
 
   // Classes with unit ("fam_") variants get both work lists (pair items and
@@ -376,6 +379,8 @@ struct eritile_gpu {
     if (cw.fam) {
       a.um = d_um.p;
       a.uw = d_uw.p;
+      a.ukprims = d_ukprims.p;
+      a.ukw = d_ukw.p;
       a.Qp = d_Qp.p;
       a.tau = tau;
     }
@@ -712,9 +717,27 @@ struct eritile_gpu {
         uw[u.prim_off + i].x = prims[pm[u.m0].prim_off + i].U;
         uw[u.prim_off + i].y = u.nm > 1 ? prims[pm[u.m1].prim_off + i].U : 0.0;
       }
+    // unit-group-transposed copy for ket reads (as build_ket_soa)
+    ukprims.assign(prims.size(), PrimRec{});
+    ukw.assign(prims.size(), double2{0.0, 0.0});
+    size_t base = 0;
+    for (const Group& g : ugroups) {
+      for (int p = 0; p < g.count; ++p) {
+        UnitMeta& u = um[g.first + p];
+        u.ksoa = static_cast<int>(base) + p;
+        u.kstride = g.count;
+        for (int j = 0; j < g.K; ++j) {
+          ukprims[base + static_cast<size_t>(j) * g.count + p] = prims[u.prim_off + j];
+          ukw[base + static_cast<size_t>(j) * g.count + p] = uw[u.prim_off + j];
+        }
+      }
+      base += static_cast<size_t>(g.K) * g.count;
+    }
     if (!host_only) {
       d_um.upload(um);
       d_uw.upload(uw);
+      d_ukprims.upload(ukprims);
+      d_ukw.upload(ukw);
       d_Qp.upload(Q.empty() ? std::vector<double>(pm.size(), 0.0) : Q);
     }
   }

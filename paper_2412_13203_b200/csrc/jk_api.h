@@ -45,8 +45,8 @@ constexpr int kBoysMmax = 16;     // slices M = 0..16 (L <= 4)
 // csrc/jk_family.cuh). Records are those of member m0; uw[prim] holds
 // (U of m0, U of m1 or 0) per primitive.
 struct alignas(16) UnitMeta {
-  int prim_off, K, nm, pad;
-  int m0, m1, pad1, pad2;  // member product pair ids
+  int prim_off, K, nm, kstride;  // kstride: ket stride in the unit-group-transposed copy
+  int m0, m1, ksoa, pad2;        // member product pair ids; first ket record in ukprims
   double ABx, ABy, ABz, pad3;
 };
 
@@ -75,6 +75,8 @@ struct LaunchArgs {
   // family (unit) launches: work items index units
   const UnitMeta* um;
   const double2* uw;     // per primitive: member weights
+  const PrimRec* ukprims;  // unit-group-transposed records (ket reads of the unit kernels)
+  const double2* ukw;      // ... and their member weights
   const double* Qp;      // Schwarz Q per product pair
   double tau;            // screening threshold (<= 0: none)
   long long seg[5];      // unit launches: item offsets of the (1,1) (1,2) (2,1) (2,2) member segments

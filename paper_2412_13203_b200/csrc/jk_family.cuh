@@ -25,14 +25,15 @@ constexpr int kFamMax = 2;  // members per unit
 template <class C, int MB, int MK, int STYLE>
 __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const double2* __restrict__ bw, int kb,
                                           const PrimRec* __restrict__ ket, const double2* __restrict__ kw, int kk,
+                                          int ks,
                                           const double* __restrict__ btab, typename C::Acc (&acc)[MB][MK]) {
 #pragma unroll
   for (int m = 0; m < MB; ++m)
 #pragma unroll
     for (int n = 0; n < MK; ++n) C::zero(acc[m][n]);
   for (int j = 0; j < kk; ++j) {
-    const PrimRec kp = load_prim<C::KPA>(ket + j);
-    const double2 kwj = __ldg(kw + j);
+    const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
+    const double2 kwj = __ldg(kw + j * ks);
     typename C::Acc s[MB];  // sum over bra prims of U_m(bra) * g, per bra member
 #pragma unroll
     for (int m = 0; m < MB; ++m) C::zero(s[m]);
@@ -121,8 +122,8 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
         bwp = sbw;
       }
     }
-    fam_drive<C, MB, MK, STYLE>(brap, bwp, bu.K, a.prims + ku.prim_off, a.uw + ku.prim_off, active ? ku.K : 0,
-                                s_boys, acc);
+    fam_drive<C, MB, MK, STYLE>(brap, bwp, bu.K, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, active ? ku.K : 0,
+                                ku.kstride, s_boys, acc);
     constexpr int nmb = MB, nmk = MK;
     const int xkey = active ? x : -1;
     const int xnext = __shfl_down_sync(0xffffffffu, xkey, 1);
