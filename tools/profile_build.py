@@ -21,6 +21,7 @@ ap.add_argument("--tau", type=float, default=1e-10)
 ap.add_argument("--builds", type=int, default=2)
 ap.add_argument("--kappa", type=float, default=1e-14)
 ap.add_argument("--tune", action="store_true")
+ap.add_argument("--set", action="append", default=[], help="CLS=VARIANT, e.g. 1000=fam_x768")
 a = ap.parse_args()
 e = Engine(0).load_molecule(water_cluster(a.waters), read_fixture("basis", a.basis)).build_pairs(a.kappa)
 e.set_screening(a.tau)
@@ -31,6 +32,12 @@ D = C @ C.T
 if a.tune:
     e.tune(D, reps=1)
     print(e.variants())
+if a.set:
+    from paper_2412_13203_b200.eritile import class_table
+    tab = ["".join(map(str, r[:4])) for r in class_table()]
+    for kv in a.set:
+        c, v = kv.split("=")
+        e.set_variant(tab.index(c), v)
 for _ in range(a.builds):
     J, K = e.build_jk(D)
 print(e.stats())
