@@ -255,6 +255,14 @@ struct eritile_gpu {
   int var_hi(int c) const { return fam_active(c) ? kClassTable[c].nvar : kClassTable[c].nvar - kClassTable[c].nfam; }
   bool uses_fam(int c) const { return fam_active(c) && variant(c) >= kClassTable[c].nvar - kClassTable[c].nfam; }
   bool active(const ClassWork& cw) const { return cw.fam == uses_fam(cw.cls); }
+  // kernels one class launch issues: unit classes launch each non-empty
+  // member segment separately
+  int kernel_launches(const ClassWork& cw) const {
+    if (!cw.fam) return 1;
+    int k = 0;
+    for (int i = 0; i < 4; ++i) k += cw.seg[i + 1] > cw.seg[i] ? 1 : 0;
+    return k;
+  }
   std::vector<int> active_work() const {
     std::vector<int> o;
     for (size_t w = 0; w < work.size(); ++w)
@@ -910,7 +918,7 @@ struct eritile_gpu {
   void launch_all(const double* dDs, double* dJK, cudaStream_t st) {
     const size_t NN = static_cast<size_t>(nbf) * nbf;
     CK(cudaMemsetAsync(dJK, 0, sizeof(double) * 2 * NN, st));
-    launches_last = 1;
+    launches_last = 0;  // kernel launches of this build (the memset is not one)
     if (profiling && prof_ev.size() < 2 * work.size()) {
       while (prof_ev.size() < 2 * work.size()) {
         cudaEvent_t e;
@@ -926,7 +934,7 @@ struct eritile_gpu {
         LaunchArgs a = class_args(cw, dDs, dJK, st);
         kClassTable[cw.cls].var[variant(cw.cls)](a);
         CK(cudaGetLastError());
-        ++launches_last;
+        launches_last += kernel_launches(cw);
         if (profiling) CK(cudaEventRecord(prof_ev[2 * w + 1], st));
       }
       return;
@@ -952,7 +960,7 @@ struct eritile_gpu {
       LaunchArgs a = class_args(cw, dDs, dJK, s);
       kClassTable[cw.cls].var[variant(cw.cls)](a);
       CK(cudaGetLastError());
-      ++launches_last;
+      launches_last += kernel_launches(cw);
     }
     for (int k = 0; k < kSide; ++k) {
       CK(cudaEventRecord(side_ev[k], side[k]));
