@@ -269,8 +269,6 @@ def variants(info) -> List[Tuple[str, str]]:
         mins = MINB_VARIANTS if info["ops"] <= MINB_SMALL_OPS else (2,)
         for m in mins:
             out.append((f"lane_m{m}", f"launch_class<Cls{cid}, {m}, kLoopPrefetch>"))
-        if info["ops"] > MINB_SMALL_OPS:
-            out.append(("lane_plm2", f"launch_class<Cls{cid}, 2, kLoopPlain>"))
         if info["ops"] > 100:
             # up to 255 registers (1 CTA of 8 warps per SM): trades occupancy
             # for the spills of the large-NV plans
@@ -279,7 +277,6 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("lane_sbm2", f"launch_class<Cls{cid}, 2, kLoopSmemBra>"))
         if info["ops"] <= MINB_SMALL_OPS:
             # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads
-            out.append(("lane_t512", f"launch_class<Cls{cid}, 1, kLoopPrefetch, 512>"))
             out.append(("lane_pl512", f"launch_class<Cls{cid}, 1, kLoopPlain, 512>"))
             out.append(("lane_pl768", f"launch_class<Cls{cid}, 1, kLoopPlain, 768>"))
             out.append(("lane_sb512", f"launch_class<Cls{cid}, 1, kLoopSmemBra, 512>"))
