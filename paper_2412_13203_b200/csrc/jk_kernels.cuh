@@ -257,7 +257,7 @@ __device__ __forceinline__ void ld_meta_late(const PairMeta* p, PairMeta& m) {
   int a, b, c, d, e, f, g, h;
   asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
   asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(e), "=r"(f), "=r"(g), "=r"(h) : "l"(reinterpret_cast<const char*>(p) + 16));
-  m.prim_off = a; m.K = b; m.bfa = c; m.bfb = d; m.sha = e; m.shb = f; m.ref = g; m.pad = h;
+  m.prim_off = a; m.K = b; m.bfa = c; m.bfb = d; m.sha = e; m.shb = f; m.ref = g; m.kstride = h;
 }
 
 // FP64 reduction into J/K. ERITILE_PROBE_NODIGEST (a measurement-only build,
