@@ -131,26 +131,45 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+FP64_DATASHEET_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+
+
 def fp64_peak():
-    """Measured FP64 FMA peak (own microbenchmark, profiles/r01_fp64_peak.json);
-    MEASURED_PEAKS.json carries no FP64 figure."""
+    """FP64 roofline denominator. MEASURED_PEAKS.json (driver-written) has no
+    FP64 entry, so this is the FP64 FMA peak measured by this repo's own
+    microbenchmark on a B200 of this pool (tools/microbench/fp64_peak.cu,
+    profiles/*fp64_peak*.json); the datasheet figure is the fallback."""
+    mp = ROOT / "MEASURED_PEAKS.json"
+    try:
+        v = json.loads(mp.read_text()).get("fp64_tflops")
+        if v:
+            return float(v), "MEASURED_PEAKS.json fp64_tflops"
+    except Exception:
+        pass
     for p in sorted((ROOT / "profiles").glob("*fp64_peak*.json")):
         try:
-            return float(json.loads(p.read_text())["fp64_fma_tflops"]), str(p.relative_to(ROOT))
+            return float(json.loads(p.read_text())["fp64_fma_tflops"]), (
+                f"{p.relative_to(ROOT)}: measured FP64 FMA peak (tools/microbench/fp64_peak.cu); "
+                "MEASURED_PEAKS.json has no FP64 entry")
         except Exception:
             pass
-    return 37.2, "fallback: B200 datasheet FP64 (148 SM x 64 DFMA x 2 x 1.965 GHz)"
+    return FP64_DATASHEET_TFLOPS, "fallback: B200 datasheet FP64 (148 SM x 64 DFMA x 2 x 1.965 GHz)"
 
 
-def ncu_traffic():
-    p = ROOT / "profiles" / "ncu_summary.json"
+def ncu_traffic(workload: str, kernel: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from an
+    `ncu --set full` capture of the same workload and kernel variant on the
+    current tree (profiles/ncu_traffic.json, written by tools/ncu_traffic.sh).
+    None when no capture matches this run's workload and kernel."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         try:
-            d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_launch"), d
+            for d in json.loads(p.read_text()):
+                if d.get("workload") == workload and d.get("kernel") == kernel:
+                    return d.get("dram_bytes_per_launch"), d.get("source")
         except Exception:
             pass
-    return None, None
+    return None, "no ncu capture of this workload/kernel on the current tree"
 
 
 # ------------------------------------------------------------------ CPU arm
@@ -220,7 +239,6 @@ def run_ours(args, rank, nranks, local_rank):
     eng.set_screening(args.tau)
     setup_s = time.perf_counter() - t0
     N = eng.nbf
-    st = eng.stats()
     Dh = synthetic_density(N, eng.nelectrons // 2)
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.Stream(dev)  # explicit stream: torch events and our kernels share it
@@ -234,12 +252,23 @@ def run_ours(args, rank, nranks, local_rank):
 
     # Workload Allocator: per-class kernel variant chosen on the live density
     # before the warm-up builds (untimed, like the reference's tune during
-    # the first SCF iterations)
+    # the first SCF iterations). Rank 0 tunes on the whole
+    # lists and broadcasts its table: the LPT deal is a function of the
+    # lists and the table, so all ranks must share it (disjoint cover).
     t1 = time.perf_counter()
-    eng.tune(Dh, reps=2)
+    table = None
+    if rank == 0:
+        eng.tune(Dh, reps=2)
+        table = eng.get_variants().tolist()
+    if dist is not None:
+        obj = [table]
+        dist.broadcast_object_list(obj, src=0)
+        table = obj[0]
+    eng.set_variants(table)
     tune_s = time.perf_counter() - t1
     chosen = eng.variants()
-    tune_table = eng.tune_times()
+    tune_table = eng.tune_times() if rank == 0 else {}
+    st = eng.stats()  # after tune: the lists and kernels the timed builds run
 
     def step():
         eng.build_jk_partial_device(D.data_ptr(), JK.data_ptr(), sp)
@@ -339,6 +368,7 @@ def run_ours(args, rank, nranks, local_rank):
     q_local = st["quartets"]
     pq_local = st["prim_quartets"]
     fl_local = st["model_flops"]
+    pair_pq, pair_fl = st["pair_path_prim_quartets"], st["pair_path_model_flops"]
     vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
     sums = torch.tensor([q_local, pq_local, fl_local], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -354,17 +384,25 @@ def run_ours(args, rank, nranks, local_rank):
     peak, peak_src = fp64_peak()
     top = max(prof, key=lambda r: r["ms"]) if prof else None
     total_prof_ms = sum(r["ms"] for r in prof) or 1.0
-    traffic, ncu = ncu_traffic()
     roof = None
     if top:
         ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
+        kern = "class (%d%d%d%d) launch, variant %s" % (*top["cls"], chosen.get(tuple(top["cls"])))
+        traffic, traffic_src = ncu_traffic(config(args, 1)["workload"], kern)
         roof = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": traffic,
-                "kernel": "class (%d%d%d%d) launch, variant %s" % (*top["cls"], chosen.get(tuple(top["cls"]))),
+                "frac_vs_datasheet": ach / FP64_DATASHEET_TFLOPS,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": kern,
                 "kernel_share_of_build": top["ms"] / total_prof_ms,
+                "kernel_timing": "CUDA events on the launch stream, one serialised profiling build (rank 0)",
+                "algorithmic_flops_per_launch": top["flops"],
                 "build_frac": (fl_tot / (ms * 1e-3) / 1e12) / (peak * nranks),
+                "build_flops_executed": fl_tot,
+                "build_flops_pair_path": pair_fl,
                 "peak_source": peak_src,
-                "flops_model": "SURVEY.md 8d: F_c = Nprim(42+3m+2(P+B+X)) + Nq(2H+12n), executed plan"}
+                "flops_model": "SURVEY.md 8d: F_c = Nprim(42+3m+2(P+B+X)) + Nq(2H+12n) with the plans and "
+                               "primitive quartets the tuned kernels execute (build_flops_executed); "
+                               "build_flops_pair_path counts the same quartets on the per-pair kernels"}
     out = {
         "metric": METRIC.format(mol=args.geom or f"(H2O)_{args.waters}", basis=args.basis, tau=args.tau), "value": q_tot / (ms * 1e-3), "unit": UNIT, "n_gpus": nranks, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -373,6 +411,7 @@ def run_ours(args, rank, nranks, local_rank):
         "s_per_build": ms * 1e-3,
         "quartets_per_build": int(q_tot), "prim_quartets_per_build": int(pq_tot),
         "prim_quartets_per_s": pq_tot / (ms * 1e-3),
+        "prim_quartets_per_build_pair_path": int(pair_pq),
         "e2e": {"value": q_tot / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 8 * N * N,
                 "d2h_bytes_per_step": 16 * N * N, "ms_per_step": e2e_ms, "api": e2e_api},
         "gpu_launches": launches * args.steps,

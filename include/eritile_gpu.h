@@ -43,6 +43,14 @@ typedef struct eritile_gpu_stats {
   double last_build_ms;      /* device time of the last build_jk (CUDA events) */
   double last_schwarz_ms;
   int gpu_launches_last_build; /* kernels launched by the last build */
+  /* Whole job (all ranks), with the variant table this context uses: */
+  long long job_quartets;
+  long long job_prim_quartets;      /* primitive quartets the chosen kernels evaluate */
+  double job_model_flops;           /* F_c over the executed plans */
+  /* The same quartets on the per-pair kernels (no shared-primitive units):
+   * the primitive-quartet count of SURVEY 8d's model. */
+  long long pair_path_prim_quartets;
+  double pair_path_model_flops;
 } eritile_gpu_stats;
 
 /* Create a context on CUDA device `device`. Fails if no device.
@@ -84,8 +92,14 @@ int eritile_gpu_schwarz(eritile_gpu* ctx, double* Q);
 /* Override Q (reference order) — used to share one Q with a checker. */
 int eritile_gpu_set_schwarz(eritile_gpu* ctx, const double* Q);
 
-/* Multi-GPU sharding: this context evaluates the work items of shard
- * `rank` of `nranks` (deterministic; set before set_screening). */
+/* Multi-GPU sharding: this context evaluates shard `rank` of
+ * `nranks`. Each class's active work list is cut into chunks of 64 warp
+ * tasks, weighted by model FLOPs, and dealt by LPT (heaviest chunk to the
+ * least-loaded rank). The deal is a function of the screened lists and the
+ * variant table only, so ranks that share both get a disjoint cover of the
+ * canonical quartet list; give every rank the same table
+ * (eritile_gpu_get_variants / eritile_gpu_set_variants). May be called
+ * before or after set_screening. */
 int eritile_gpu_set_shard(eritile_gpu* ctx, int rank, int nranks);
 /* Build the screened quartet work lists: keep (x,y) iff Q_x*Q_y >= tau
  * (tau <= 0: no screening). Blocks are class- and contraction-sorted
@@ -95,6 +109,11 @@ long long eritile_gpu_num_quartets(const eritile_gpu* ctx);
 /* Export this rank's canonical quartet list as reference pair-store index
  * pairs (x <= y), sorted ascending by (x, y). Returns the count. */
 long long eritile_gpu_quartets(const eritile_gpu* ctx, int* xs, int* ys, long long cap);
+/* Compact list identity for lists too large to export: per reference pair x
+ * (npairs entries), the number of this rank's canonical quartets (x, y),
+ * x <= y, and the wrapping 64-bit sum of splitmix64(y) over them. Returns
+ * the total count (-1 on error). */
+long long eritile_gpu_pair_survivors(const eritile_gpu* ctx, long long* count, unsigned long long* ysum);
 
 /* build_g's J/K half: true Coulomb J and exchange K for a
  * symmetric density D (G = 2J - K for RHF). Host buffers; includes H2D of D
@@ -130,16 +149,22 @@ int eritile_gpu_set_profiling(eritile_gpu* ctx, int on);
 int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, double* flops,
                               long long* quartets, long long* prim_quartets);
 /* Workload Allocator (Alg. 2; SPEC.md:367-438 tune): time
- * every kernel variant of every class launch of this rank on density D
- * (host, N x N), median of `reps` launches each, and keep the fastest per
- * class. Variants: "lane_m2"/"lane_m3" (one lane per quartet, straight-line
- * plan, residency target 2/3 CTAs per SM) and "coop" (CTA-cooperative
- * level-scheduled plan). The choice changes atomic summation order only. */
+ * every kernel variant of every class on its whole (unsharded) work list on
+ * density D (host, N x N), median of `reps` launches each, and keep the
+ * fastest per class. Variant families (eritile_gpu_variant_name):
+ * "lane_*" one lane per contracted quartet running the class's straight-line
+ * plan (loop style x CTA shape x register budget), "fam_*" the same over
+ * shared-primitive units, "coop"/"coopw" the CTA-/warp-cooperative
+ * level-scheduled plan. The choice changes atomic summation order only. */
 int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps);
-/* Per class launch of the last tune: class table index and the median ms of
- * each variant (kMaxVariants = 12 per launch, 0 = no such variant). */
+/* Per class of the last tune: class table index and the median ms of each
+ * variant (kMaxVariants = 16 per class, 0 = not timed). */
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms);
 int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var);
+/* The whole variant table (one entry per class, eritile_gpu_num_classes):
+ * get returns the class count; set validates every entry first. */
+int eritile_gpu_get_variants(const eritile_gpu* ctx, int* var, int cap);
+int eritile_gpu_set_variants(eritile_gpu* ctx, const int* var, int n);
 /* Shared-primitive units (generally contracted sibling shells evaluated once
  * per primitive quartet, csrc/jk_family.cuh): on by default; classes with
  * "fam_" variants then run only those. Takes effect at the next

@@ -751,6 +751,10 @@ typedef struct {
   double** Kp;
   long long* nq;
   int mode; /* 0 = Q, 1 = JK */
+  const unsigned char* nzb; /* D-sparse builds: per shell pair (s*nshell+t), D block nonzero */
+  const int* lx;            /* explicit quartet list (build_jk_list), else NULL */
+  const int* ly;
+  long long nlist;
 } job_t;
 
 typedef struct {
@@ -886,6 +890,15 @@ static void digest(const orc_ctx* C, int x, int y, const double* v, const double
         }
 }
 
+/* D-sparse skip (orc_build_jk_dsparse): every one of the six D blocks the
+ * quartet reads is zero, so its J/K contributions are exactly zero. */
+static int d_blocks_zero(const orc_ctx* C, const unsigned char* nzb, int x, int y) {
+  const int S = C->nshell;
+  const int i = C->pr[x].i, j = C->pr[x].j, k = C->pr[y].i, l = C->pr[y].j;
+  return !(nzb[k * S + l] | nzb[i * S + j] | nzb[j * S + l] | nzb[i * S + k] | nzb[j * S + k] |
+           nzb[i * S + l]);
+}
+
 static void* jk_worker(void* arg) {
   warg_t* wa = arg;
   job_t* J = wa->job;
@@ -906,6 +919,7 @@ static void* jk_worker(void* arg) {
       int y0 = C->bl[bi].bt == C->bl[bi].kt ? x : tj->first;
       for (int y = y0; y < tj->first + tj->count; ++y) {
         if (!keep(C, J->tau, x, y)) continue;
+        if (J->nzb && d_blocks_zero(C, J->nzb, x, y)) continue;
         eri_scaled(C, x, y, &S, out);
         digest(C, x, y, out, J->D, J->Jp[wa->w], J->Kp[wa->w]);
         ++nq;
@@ -922,9 +936,167 @@ static void* jk_worker(void* arg) {
   return NULL;
 }
 
+/* Worker over an explicit canonical quartet list (x <= y), 1024 at a time. */
+static void* jk_list_worker(void* arg) {
+  warg_t* wa = arg;
+  job_t* J = wa->job;
+  orc_ctx* C = J->C;
+  scratch_t S;
+  memset(&S, 0, sizeof S);
+  double* out = malloc(sizeof(double) * 50625);
+  long long nq = 0;
+  for (;;) {
+    const long long b = 1024 * __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+    if (b >= J->nlist) break;
+    const long long e = b + 1024 < J->nlist ? b + 1024 : J->nlist;
+    for (long long q = b; q < e; ++q) {
+      eri_scaled(C, J->lx[q], J->ly[q], &S, out);
+      digest(C, J->lx[q], J->ly[q], out, J->D, J->Jp[wa->w], J->Kp[wa->w]);
+      ++nq;
+    }
+  }
+  J->nq[wa->w] = nq;
+  free(out);
+  free(S.V);
+  free(S.Cc);
+  free(S.HB);
+  free(S.HK);
+  free(S.raw);
+  return NULL;
+}
+
+static int jk_run(orc_ctx* C, const double* D, double tau, int nthreads, long long stride,
+                  long long offset, const unsigned char* nzb, const int* lx, const int* ly,
+                  long long nlist, double* Jout, double* Kout, long long* nquartets, double* seconds);
+
 int orc_build_jk_timed(orc_ctx* C, const double* D, double tau, int nthreads, long long stride,
                        long long offset, double* Jout, double* Kout, long long* nquartets,
                        double* seconds) {
+  return jk_run(C, D, tau, nthreads, stride, offset, NULL, NULL, NULL, 0, Jout, Kout, nquartets, seconds);
+}
+
+int orc_build_jk_dsparse(orc_ctx* C, const double* D, double tau, int nthreads, double* Jout,
+                         double* Kout, long long* nquartets) {
+  pthread_once(&g_once, init_tables);
+  const int S = C->nshell;
+  const size_t N = (size_t)C->nbf;
+  unsigned char* nzb = calloc((size_t)S * (size_t)S, 1);
+  for (int s = 0; s < S; ++s)
+    for (int t = 0; t < S; ++t) {
+      const int ns = ncart(C->sh[s].L), nt = ncart(C->sh[t].L);
+      unsigned char nz = 0;
+      for (int m = 0; m < ns && !nz; ++m)
+        for (int n = 0; n < nt; ++n)
+          if (D[(size_t)(C->bf_off[s] + m) * N + (size_t)(C->bf_off[t] + n)] != 0.0) {
+            nz = 1;
+            break;
+          }
+      nzb[s * S + t] = nz;
+    }
+  const int rc = jk_run(C, D, tau, nthreads, 1, 0, nzb, NULL, NULL, 0, Jout, Kout, nquartets, NULL);
+  free(nzb);
+  return rc;
+}
+
+int orc_build_jk_list(orc_ctx* C, const double* D, long long n, const int* xs, const int* ys,
+                      int nthreads, double* Jout, double* Kout) {
+  for (long long q = 0; q < n; ++q)
+    if (xs[q] < 0 || ys[q] < xs[q] || ys[q] >= C->npair) {
+      set_err("build_jk_list: quartets must be canonical pair-store indices x <= y < npairs");
+      return -1;
+    }
+  return jk_run(C, D, 0.0, nthreads, 1, 0, NULL, xs, ys, n, Jout, Kout, NULL, NULL);
+}
+
+/* Per pair x: canonical survivors (x, y >= x) in block order and the wrapping
+ * sum of splitmix64(y) (compact list identity at sizes too large to export). */
+typedef struct {
+  orc_ctx* C;
+  double tau;
+  long long next;
+  long long** cnt;
+  unsigned long long** hs;
+} surv_job_t;
+typedef struct {
+  surv_job_t* job;
+  int w;
+} surv_arg_t;
+static unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+static void* surv_worker(void* arg) {
+  surv_arg_t* a = arg;
+  surv_job_t* J = a->job;
+  const orc_ctx* C = J->C;
+  long long* cn = J->cnt[a->w];
+  unsigned long long* hs = J->hs[a->w];
+  for (;;) {
+    const long long bi = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+    if (bi >= C->nblock) break;
+    const tile_t* ti = &C->tl[C->bl[bi].bt];
+    const tile_t* tj = &C->tl[C->bl[bi].kt];
+    for (int x = ti->first; x < ti->first + ti->count; ++x) {
+      int y0 = C->bl[bi].bt == C->bl[bi].kt ? x : tj->first;
+      for (int y = y0; y < tj->first + tj->count; ++y)
+        if (keep(C, J->tau, x, y)) {
+          ++cn[x];
+          hs[x] += splitmix64((unsigned long long)y);
+        }
+    }
+  }
+  return NULL;
+}
+long long orc_pair_survivors(orc_ctx* C, double tau, long long* count, unsigned long long* ysum) {
+  pthread_once(&g_once, init_tables);
+  if (tau > 0.0) compute_q(C);
+  const int nt = default_threads();
+  surv_job_t J;
+  memset(&J, 0, sizeof J);
+  J.C = C;
+  J.tau = tau;
+  J.cnt = malloc(sizeof(long long*) * (size_t)nt);
+  J.hs = malloc(sizeof(unsigned long long*) * (size_t)nt);
+  for (int w = 0; w < nt; ++w) {
+    J.cnt[w] = calloc((size_t)C->npair, sizeof(long long));
+    J.hs[w] = calloc((size_t)C->npair, sizeof(unsigned long long));
+  }
+  pthread_t* th = malloc(sizeof(pthread_t) * (size_t)nt);
+  surv_arg_t* wa = malloc(sizeof(surv_arg_t) * (size_t)nt);
+  for (int w = 0; w < nt; ++w) {
+    wa[w].job = &J;
+    wa[w].w = w;
+    pthread_create(&th[w], NULL, surv_worker, &wa[w]);
+  }
+  for (int w = 0; w < nt; ++w) pthread_join(th[w], NULL);
+  long long total = 0;
+  for (int x = 0; x < C->npair; ++x) {
+    long long c = 0;
+    unsigned long long h = 0;
+    for (int w = 0; w < nt; ++w) {
+      c += J.cnt[w][x];
+      h += J.hs[w][x];
+    }
+    count[x] = c;
+    ysum[x] = h;
+    total += c;
+  }
+  for (int w = 0; w < nt; ++w) {
+    free(J.cnt[w]);
+    free(J.hs[w]);
+  }
+  free(J.cnt);
+  free(J.hs);
+  free(th);
+  free(wa);
+  return total;
+}
+
+static int jk_run(orc_ctx* C, const double* D, double tau, int nthreads, long long stride,
+                  long long offset, const unsigned char* nzb, const int* lx, const int* ly,
+                  long long nlist, double* Jout, double* Kout, long long* nquartets, double* seconds) {
   pthread_once(&g_once, init_tables);
   if (tau > 0.0) compute_q(C);
   if (nthreads <= 0) nthreads = default_threads();
@@ -937,6 +1109,10 @@ int orc_build_jk_timed(orc_ctx* C, const double* D, double tau, int nthreads, lo
   J.stride = stride;
   J.offset = offset;
   J.nthreads = nthreads;
+  J.nzb = nzb;
+  J.lx = lx;
+  J.ly = ly;
+  J.nlist = nlist;
   J.Jp = malloc(sizeof(double*) * (size_t)nthreads);
   J.Kp = malloc(sizeof(double*) * (size_t)nthreads);
   J.nq = calloc((size_t)nthreads, sizeof(long long));
@@ -946,7 +1122,7 @@ int orc_build_jk_timed(orc_ctx* C, const double* D, double tau, int nthreads, lo
   }
   struct timespec t0, t1;
   clock_gettime(CLOCK_MONOTONIC, &t0);
-  run_workers(&J, jk_worker);
+  run_workers(&J, lx ? jk_list_worker : jk_worker);
   clock_gettime(CLOCK_MONOTONIC, &t1);
   if (seconds) *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
   double* Jm = calloc(NN, sizeof(double));

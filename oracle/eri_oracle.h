@@ -57,6 +57,17 @@ int orc_build_jk_sample(orc_ctx* c, const double* D, double tau, int nthreads,
  * phase only (excludes partial-matrix allocation and merge). */
 int orc_build_jk_timed(orc_ctx* c, const double* D, double tau, int nthreads, long long stride,
                        long long offset, double* J, double* K, long long* nquartets, double* seconds);
+/* D-sparse build: as build_jk, but quartets whose six D blocks are all zero
+ * are skipped (their contributions are exactly zero); *nquartets counts the
+ * evaluated ones. Makes full-size parity checks cheap with a sparse D. */
+int orc_build_jk_dsparse(orc_ctx* c, const double* D, double tau, int nthreads, double* J,
+                         double* K, long long* nquartets);
+/* J/K over an explicit canonical quartet list (x <= y, pair-store indices). */
+int orc_build_jk_list(orc_ctx* c, const double* D, long long n, const int* xs, const int* ys,
+                      int nthreads, double* J, double* K);
+/* Per pair x: surviving canonical quartets (x, y >= x) and the wrapping sum
+ * of splitmix64(y) over them; returns the total. */
+long long orc_pair_survivors(orc_ctx* c, double tau, long long* count, unsigned long long* ysum);
 /* One-electron S, T, V, McMurchie-Davidson; scaled. */
 int orc_one_electron(orc_ctx* c, double* S, double* T, double* V);
 double orc_nuclear_repulsion(orc_ctx* c);

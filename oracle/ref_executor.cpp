@@ -132,6 +132,16 @@ void eval_quartet(const ShellPair& b, const ShellPair& k, const ExecutionPlan& P
   for (std::size_t n = 0; n < P.targets.size(); ++n) out[n] = t[P.targets[n]];
 }
 
+// Component scales per L, built once (no per-quartet allocation).
+const std::vector<double>& scales_of(int L) {
+  static const std::vector<std::vector<double>> tab = [] {
+    std::vector<std::vector<double>> t;
+    for (int l = 0; l <= 6; ++l) t.push_back(comp_scales(l));
+    return t;
+  }();
+  return tab.at(static_cast<std::size_t>(L));
+}
+
 struct Scratch {
   std::vector<double> r, t, F, v;
 };
@@ -144,8 +154,8 @@ void quartet_scaled(Ctx& C, int x, int y, Scratch& S) {
   const ExecutionPlan& P = C.plan(cls);
   S.v.resize(P.targets.size());
   eval_quartet(b, k, P, S.r, S.t, S.F, S.v.data());
-  auto si = comp_scales(cls.la), sj = comp_scales(cls.lb), sk = comp_scales(cls.lc),
-       sl = comp_scales(cls.ld);
+  const std::vector<double>&si = scales_of(cls.la), &sj = scales_of(cls.lb), &sk = scales_of(cls.lc),
+                           &sl = scales_of(cls.ld);
   std::size_t n = 0;
   for (double a : si)
     for (double bb : sj)
@@ -452,6 +462,54 @@ int ref_build_jk_timed(void* cv, const double* D, double tau, int nthreads, long
     g_err = e.what();
     return -1;
   }
+}
+
+// Per pair x: canonical survivors (x, y >= x) in block order (block.hpp:
+// 135-150) and the wrapping sum of splitmix64(y) over them - list identity at
+// sizes too large to export. Returns the total.
+long long ref_pair_survivors(void* cv, double tau, long long* count, unsigned long long* ysum) {
+  Ctx* C = static_cast<Ctx*>(cv);
+  try {
+    if (tau > 0.0) compute_q(*C);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+  const std::size_t np = C->pairs.size();
+  const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  std::vector<std::vector<long long>> cn(nt, std::vector<long long>(np, 0));
+  std::vector<std::vector<unsigned long long>> hs(nt, std::vector<unsigned long long>(np, 0));
+  auto mix = [](unsigned long long z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  std::atomic<long long> next{0};
+  const long long nb = static_cast<long long>(C->blocks.size());
+  std::vector<std::thread> th;
+  for (unsigned w = 0; w < nt; ++w)
+    th.emplace_back([&, w] {
+      for (long long bi; (bi = next.fetch_add(1)) < nb;)
+        for_each_quartet_in_block(*C, C->blocks[bi], tau, [&](int x, int y) {
+          ++cn[w][x];
+          hs[w][x] += mix(static_cast<unsigned long long>(y));
+        });
+    });
+  for (auto& t : th) t.join();
+  long long total = 0;
+  for (std::size_t x = 0; x < np; ++x) {
+    long long c = 0;
+    unsigned long long h = 0;
+    for (unsigned w = 0; w < nt; ++w) {
+      c += cn[w][x];
+      h += hs[w][x];
+    }
+    count[x] = c;
+    ysum[x] = h;
+    total += c;
+  }
+  return total;
 }
 
 void ref_boys(int m, double T, double* F) { boys_inplace(m, T, F); }

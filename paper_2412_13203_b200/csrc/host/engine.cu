@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -24,6 +25,7 @@
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../../include/eritile_gpu.h"
@@ -63,9 +65,19 @@ struct DevBuf {
     CK(cudaMalloc(&p, sizeof(T) * count));
     n = count;
   }
-  void upload(const std::vector<T>& v) {
+  // Stream-ordered and complete on return: a pageable cudaMemcpy may return
+  // before its DMA lands, and kernels on a non-blocking stream would not wait
+  // for it.
+  void upload(const std::vector<T>& v, cudaStream_t st) {
     alloc(v.size());
-    if (!v.empty()) CK(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    if (v.empty()) return;
+    CK(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  void download(T* dst, size_t count, cudaStream_t st) const {
+    if (count == 0) return;
+    CK(cudaMemcpyAsync(dst, p, sizeof(T) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
   }
   void release() {
     if (p) cudaFree(p);
@@ -175,14 +187,23 @@ struct Group {
   int nm = 1;        // unit groups: members per unit
 };
 
+// One class work list. The full (unsharded) list lives in all_items at
+// [aoff, aoff + an); this rank's share (the LPT deal, eritile_gpu::deal) is
+// [off, off + n) of the rank-local list. Unit classes keep their (1,1)
+// (1,2) (2,1) (2,2) member segments contiguous in both (seg relative to off).
 struct ClassWork {
   int cls;  // index into kClassTable
   bool fam; // items index units (shared-primitive kernels)
-  long long off, n;
-  long long seg[5] = {0, 0, 0, 0, 0};  // unit classes: (1,1)(1,2)(2,1)(2,2) member segments, relative
-  long long quartets, prim_quartets;
-  double flops = 0.0;    // model FLOPs of this class launch
+  long long aoff = 0, an = 0;
+  long long aseg[5] = {0, 0, 0, 0, 0};
+  long long aquartets = 0, aprim = 0;
+  double cost_prim = 0.0, cost_q = 0.0;  // model FLOPs per primitive / contracted quartet
+  long long off = 0, n = 0;
+  long long seg[5] = {0, 0, 0, 0, 0};
+  long long quartets = 0, prim_quartets = 0;
+  double flops = 0.0;    // model FLOPs of this rank's launch
   double last_ms = 0.0;  // device time of the last launch (profiling mode)
+  double full_flops() const { return cost_prim * static_cast<double>(aprim) + cost_q * static_cast<double>(aquartets); }
 };
 
 }  // namespace eritile_b200
@@ -216,9 +237,13 @@ struct eritile_gpu {
   int rank = 0, nranks = 1;
   double tau = 0.0;
 
-  std::vector<WorkItem> items;
+  std::vector<WorkItem> all_items;        // every class list, unsharded
+  std::vector<unsigned char> item_q;      // contracted quartets per item (all_items)
+  std::vector<unsigned> item_p;           // primitive quartets per item (all_items)
+  std::vector<WorkItem> items;            // this rank's items (nranks > 1)
   std::vector<int> cnt;  // survivor counts per (group pair, bra) + sentinel
   std::vector<ClassWork> work;
+  bool dealt = false;   // rank-local lists match the current variants and shard
   long long quartets = 0, prim_quartets = 0;
   double model_flops = 0.0;
   double last_build_ms = 0.0, last_schwarz_ms = 0.0;
@@ -227,7 +252,7 @@ struct eritile_gpu {
   DevBuf<PairMeta> d_pm;
   DevBuf<PrimRec> d_prims, d_kprims;
   DevBuf<double> d_boys, d_scale, d_Q;
-  DevBuf<WorkItem> d_items;
+  DevBuf<WorkItem> d_all_items, d_items;
   DevBuf<int> d_cnt;
   DevBuf<int> d_list;
   DevBuf<double> d_D, d_Ds, d_JK, d_J, d_K;
@@ -343,7 +368,7 @@ struct eritile_gpu {
         if (w < 0) continue;
         std::vector<double> t;
         for (int r = 0; r < reps + 1; ++r) {
-          LaunchArgs a = class_args(work[w], dDs, scratch.p, stream);
+          LaunchArgs a = class_args(work[w], dDs, scratch.p, stream, true);
           CK(cudaEventRecord(e0, stream));
           ce.var[v](a);
           CK(cudaGetLastError());
@@ -361,17 +386,21 @@ struct eritile_gpu {
       }
       var_choice[c] = bestv;
     }
-    update_totals();
+    dealt = false;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
 
-  LaunchArgs class_args(const ClassWork& cw, const double* dDs, double* dJK, cudaStream_t st) const {
+  // full = true: the class's whole (unsharded) list (the allocator times
+  // those); else this rank's share.
+  LaunchArgs class_args(const ClassWork& cw, const double* dDs, double* dJK, cudaStream_t st,
+                        bool full = false) const {
     const size_t NN = static_cast<size_t>(nbf) * nbf;
     LaunchArgs a{};
     a.mode = 0;
-    a.items = d_items.p + cw.off;
-    a.nitems = cw.n;
+    const bool use_all = full || nranks == 1;
+    a.items = use_all ? d_all_items.p + cw.aoff : d_items.p + cw.off;
+    a.nitems = full ? cw.an : cw.n;
     a.cnt = d_cnt.p;
     a.pm = d_pm.p;
     a.prims = d_prims.p;
@@ -383,7 +412,7 @@ struct eritile_gpu {
     a.boys_tab = d_boys.p;
     a.stream = st;
     a.block = 128;
-    for (int k = 0; k < 5; ++k) a.seg[k] = cw.seg[k];
+    for (int k = 0; k < 5; ++k) a.seg[k] = full ? cw.aseg[k] : cw.seg[k];
     if (cw.fam) {
       a.um = d_um.p;
       a.uw = d_uw.p;
@@ -433,7 +462,8 @@ struct eritile_gpu {
     }
     have_mol = true;
     have_pairs = have_q = have_lists = false;
-    if (!host_only) d_scale.upload(bf_scale);
+    Q.clear();  // Q belongs to the previous pair store
+    if (!host_only) d_scale.upload(bf_scale, stream);
   }
 
   // block.hpp:52-103 restated + product orientation and grouping.
@@ -547,11 +577,12 @@ struct eritile_gpu {
       groups.back().count++;
     }
     if (!host_only) {
-      d_pm.upload(pm);
-      d_prims.upload(prims);
+      d_pm.upload(pm, stream);
+      d_prims.upload(prims, stream);
     }
     have_pairs = true;
     have_q = have_lists = false;
+    Q.clear();  // Q belongs to the previous pair store
   }
 
   double elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -576,7 +607,7 @@ struct eritile_gpu {
           for (int x = g.first; x < g.first + g.count; ++x) list.push_back(x);
       if (list.empty()) continue;
       DevBuf<int> dl;
-      dl.upload(list);
+      dl.upload(list, stream);
       LaunchArgs a{};
       a.mode = 1;
       a.pair_list = dl.p;
@@ -595,7 +626,7 @@ struct eritile_gpu {
     CK(cudaEventSynchronize(ev1));
     last_schwarz_ms = elapsed(ev0, ev1);
     Q.resize(np);
-    CK(cudaMemcpy(Q.data(), d_Q.p, sizeof(double) * np, cudaMemcpyDeviceToHost));
+    d_Q.download(Q.data(), np, stream);
     have_q = true;
     have_lists = false;
   }
@@ -638,8 +669,8 @@ struct eritile_gpu {
     }
     prims.swap(nprims);
     if (!host_only) {
-      d_pm.upload(pm);
-      d_prims.upload(prims);
+      d_pm.upload(pm, stream);
+      d_prims.upload(prims, stream);
     }
   }
 
@@ -659,8 +690,8 @@ struct eritile_gpu {
       base += static_cast<size_t>(g.K) * g.count;
     }
     if (!host_only) {
-      d_pm.upload(pm);
-      d_kprims.upload(kprims);
+      d_pm.upload(pm, stream);
+      d_kprims.upload(kprims, stream);
     }
   }
 
@@ -742,11 +773,11 @@ struct eritile_gpu {
       base += static_cast<size_t>(g.K) * g.count;
     }
     if (!host_only) {
-      d_um.upload(um);
-      d_uw.upload(uw);
-      d_ukprims.upload(ukprims);
-      d_ukw.upload(ukw);
-      d_Qp.upload(Q.empty() ? std::vector<double>(pm.size(), 0.0) : Q);
+      d_um.upload(um, stream);
+      d_uw.upload(uw, stream);
+      d_ukprims.upload(ukprims, stream);
+      d_ukw.upload(ukw, stream);
+      d_Qp.upload(Q.empty() ? std::vector<double>(pm.size(), 0.0) : Q, stream);
     }
   }
 
@@ -810,6 +841,9 @@ struct eritile_gpu {
       if (a.seg != b.seg) return a.seg < b.seg;
       return a.cost > b.cost;
     });
+    all_items.clear();
+    item_q.clear();
+    item_p.clear();
     items.clear();
     work.clear();
     cnt.clear();
@@ -818,11 +852,13 @@ struct eritile_gpu {
     for (size_t s = 0; s < gps.size();) {
       const int cls = gps[s].cls;
       const bool fam = gps[s].fam;
-      ClassWork cw{cls, fam, static_cast<long long>(items.size()), 0, {0, 0, 0, 0, 0}, 0, 0, 0.0, 0.0};
-      long long counter = 0;  // warp-task counter within the class (sharding)
+      ClassWork cw{};
+      cw.cls = cls;
+      cw.fam = fam;
+      cw.aoff = static_cast<long long>(all_items.size());
       int cur_seg = 0;
       for (; s < gps.size() && gps[s].cls == cls && gps[s].fam == fam; ++s) {
-        while (cur_seg < gps[s].seg) cw.seg[++cur_seg] = static_cast<long long>(items.size()) - cw.off;
+        while (cur_seg < gps[s].seg) cw.aseg[++cur_seg] = static_cast<long long>(all_items.size()) - cw.aoff;
         const Group& gx = fam ? ugroups[gps[s].X] : groups[gps[s].X];
         const Group& gy = fam ? ugroups[gps[s].Y] : groups[gps[s].Y];
         const std::vector<double>& QQ = fam ? uQ : Q;
@@ -851,61 +887,155 @@ struct eritile_gpu {
         // cut the flat sequence into warp tasks of 32 (unit) quartets
         int r = 0;      // current bra rank within gx
         long long off = 0;  // offset within bra r's survivors
-        for (long long base = 0; base < total; base += 32, ++counter) {
+        for (long long base = 0; base < total; base += 32) {
           while (r < gx.count && off >= cnt[cbase + r]) {
             off -= cnt[cbase + r];
             ++r;
           }
           const int nq = static_cast<int>(std::min<long long>(32, total - base));
-          if (counter % nranks == rank) {
-            items.push_back(WorkItem{gx.first + r, static_cast<int>(off) | (nq << 24), cbase + r, gy.first});
-            cw.prim_quartets += static_cast<long long>(nq) * gx.K * gy.K;
-            if (!fam) {
-              cw.quartets += nq;
-            } else {  // member quartets of these nq unit pairs
-              int rr = r, oo = static_cast<int>(off);
-              for (int l = 0; l < nq; ++l, ++oo) {
-                while (oo >= cnt[cbase + rr]) {
-                  oo -= cnt[cbase + rr];
-                  ++rr;
-                }
-                cw.quartets += unit_pair_quartets(gx.first + rr, gy.first + oo, t);
+          all_items.push_back(WorkItem{gx.first + r, static_cast<int>(off) | (nq << 24), cbase + r, gy.first});
+          int q = nq;
+          if (fam) {  // member quartets of these nq unit pairs
+            q = 0;
+            int rr = r, oo = static_cast<int>(off);
+            for (int l = 0; l < nq; ++l, ++oo) {
+              while (oo >= cnt[cbase + rr]) {
+                oo -= cnt[cbase + rr];
+                ++rr;
               }
+              q += unit_pair_quartets(gx.first + rr, gy.first + oo, t);
             }
           }
+          item_q.push_back(static_cast<unsigned char>(q));
+          item_p.push_back(static_cast<unsigned>(nq * gx.K * gy.K));
+          cw.aquartets += q;
+          cw.aprim += static_cast<long long>(nq) * gx.K * gy.K;
           off += 32;
         }
       }
-      cw.n = static_cast<long long>(items.size()) - cw.off;
-      while (cur_seg < 4) cw.seg[++cur_seg] = cw.n;
-      if (std::getenv("ERITILE_DEBUG_ITEMS") && cw.n > 0) {  // diagnostics: items spanning > 1 bra
+      cw.an = static_cast<long long>(all_items.size()) - cw.aoff;
+      while (cur_seg < 4) cw.aseg[++cur_seg] = cw.an;
+      if (std::getenv("ERITILE_DEBUG_ITEMS") && cw.an > 0) {  // diagnostics: items spanning > 1 bra
         long long multi = 0;
-        for (long long w = cw.off; w < cw.off + cw.n; ++w) {
-          const WorkItem& it = items[w];
+        for (long long w = cw.aoff; w < cw.aoff + cw.an; ++w) {
+          const WorkItem& it = all_items[w];
           if ((it.r0nq & 0xffffff) + (it.r0nq >> 24) > cnt[it.cntp]) ++multi;
         }
-        std::fprintf(stderr, "class %d fam %d items %lld multi-bra %.3f\n", cls, fam ? 1 : 0, cw.n,
-                     static_cast<double>(multi) / cw.n);
+        std::fprintf(stderr, "class %d fam %d items %lld multi-bra %.3f\n", cls, fam ? 1 : 0, cw.an,
+                     static_cast<double>(multi) / cw.an);
       }
-      if (cw.n > 0) {
+      if (cw.an > 0) {
         const ClassEntry& ce = kClassTable[cls];
         const double nv = static_cast<double>((ce.la + 1) * (ce.la + 2) / 2 * (ce.lb + 1) * (ce.lb + 2) / 2 *
                                               (ce.lc + 1) * (ce.lc + 2) / 2 * (ce.ld + 1) * (ce.ld + 2) / 2);
         // F_c = Nprim (42 + 3m + 2(P+B+X)) + Nq (2H + 12 n), with
         // P, B, X, H from the plan this kernel executes; Nprim counts the
         // primitive quartets actually evaluated (once per unit pair).
-        cw.flops = static_cast<double>(cw.prim_quartets) *
-                       (42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract)) +
-                   static_cast<double>(cw.quartets) * (2.0 * ce.hrr_terms + 12.0 * nv);
+        cw.cost_prim = 42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract);
+        cw.cost_q = 2.0 * ce.hrr_terms + 12.0 * nv;
         work.push_back(cw);
       }
     }
-    update_totals();
     if (!host_only) {
-      d_cnt.upload(cnt);
-      d_items.upload(items);
+      d_cnt.upload(cnt, stream);
+      d_all_items.upload(all_items, stream);
     }
     have_lists = true;
+    dealt = false;
+    deal();
+  }
+
+  // Quartet-block sharding (quartets are independent,
+  // block.hpp:40-42): the active list of every class is cut into chunks of
+  // kDealChunk warp tasks (never across a unit member segment), each weighted
+  // by its model FLOPs (SURVEY 8d F_c: primitive and contracted quartets of
+  // its items), and the chunks are dealt by LPT - heaviest first, each to the
+  // least-loaded rank, ties to the lower rank and the lower chunk index. The
+  // deal depends only on the lists and the variant table, so every rank
+  // computes the same one and the shards are a disjoint cover of the
+  // canonical list, PROVIDED all ranks use the same variant table
+  // (variant_signature; bench.py broadcasts rank 0's tuned table). A rank's
+  // items of a class keep chunk order (Q-sorted locality).
+  static constexpr long long kDealChunk = 64;
+  void deal() {
+    if (!have_lists) return;
+    if (nranks == 1) {
+      for (ClassWork& cw : work) {
+        cw.off = cw.aoff;
+        cw.n = cw.an;
+        for (int k = 0; k < 5; ++k) cw.seg[k] = cw.aseg[k];
+        cw.quartets = cw.aquartets;
+        cw.prim_quartets = cw.aprim;
+        cw.flops = cw.full_flops();
+      }
+      items.clear();
+      update_totals();
+      dealt = true;
+      return;
+    }
+    struct Chunk {
+      long long b, e;  // all_items range
+      double w;
+      int owner;
+    };
+    std::vector<Chunk> ch;
+    std::vector<std::pair<size_t, size_t>> wch(work.size(), {0, 0});  // chunk range per work entry
+    for (size_t w = 0; w < work.size(); ++w) {
+      const ClassWork& cw = work[w];
+      wch[w].first = ch.size();
+      if (active(cw)) {
+        const int nseg = cw.fam ? 4 : 1;
+        for (int sg = 0; sg < nseg; ++sg) {
+          const long long s0 = cw.aoff + (cw.fam ? cw.aseg[sg] : 0);
+          const long long s1 = cw.aoff + (cw.fam ? cw.aseg[sg + 1] : cw.an);
+          for (long long b = s0; b < s1; b += kDealChunk) {
+            const long long e = std::min(s1, b + kDealChunk);
+            double wt = 0.0;
+            for (long long i = b; i < e; ++i) wt += cw.cost_prim * item_p[i] + cw.cost_q * item_q[i];
+            ch.push_back(Chunk{b, e, wt, 0});
+          }
+        }
+      }
+      wch[w].second = ch.size();
+    }
+    std::vector<size_t> ord(ch.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ch[a].w > ch[b].w; });
+    std::vector<double> load(nranks, 0.0);
+    for (size_t k : ord) {
+      int r = 0;
+      for (int q = 1; q < nranks; ++q)
+        if (load[q] < load[r]) r = q;
+      ch[k].owner = r;
+      load[r] += ch[k].w;
+    }
+    items.clear();
+    for (size_t w = 0; w < work.size(); ++w) {
+      ClassWork& cw = work[w];
+      cw.off = static_cast<long long>(items.size());
+      cw.quartets = cw.prim_quartets = 0;
+      for (int k = 0; k < 5; ++k) cw.seg[k] = 0;
+      int sg = 0;
+      for (size_t k = wch[w].first; k < wch[w].second; ++k) {
+        const Chunk& c = ch[k];
+        while (cw.fam && sg < 4 && c.b - cw.aoff >= cw.aseg[sg + 1]) cw.seg[++sg] = static_cast<long long>(items.size()) - cw.off;
+        if (c.owner != rank) continue;
+        for (long long i = c.b; i < c.e; ++i) {
+          items.push_back(all_items[i]);
+          cw.quartets += item_q[i];
+          cw.prim_quartets += item_p[i];
+        }
+      }
+      cw.n = static_cast<long long>(items.size()) - cw.off;
+      while (sg < 4) cw.seg[++sg] = cw.n;
+      cw.flops = cw.cost_prim * static_cast<double>(cw.prim_quartets) + cw.cost_q * static_cast<double>(cw.quartets);
+    }
+    if (!host_only) d_items.upload(items, stream);
+    update_totals();
+    dealt = true;
+  }
+  void ensure_dealt() {
+    if (have_lists && !dealt) deal();
   }
 
   void ensure_mats() {
@@ -990,9 +1120,88 @@ struct eritile_gpu {
     CK(cudaGetLastError());
   }
 
+  // Per reference pair x: count and splitmix64 sum of y over this rank's
+  // canonical quartets (x, y), x <= y (eritile_gpu_pair_survivors).
+  long long pair_survivors(long long* count, unsigned long long* ysum) const {
+    const size_t np = pm.size();
+    std::vector<std::pair<const ClassWork*, long long>> jobs;  // (class list, first local item)
+    for (const ClassWork& cw : work)
+      if (active(cw))
+        for (long long b = 0; b < cw.n; b += 4096) jobs.emplace_back(&cw, b);
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::vector<long long>> tc(nt, std::vector<long long>(np, 0));
+    std::vector<std::vector<unsigned long long>> th(nt, std::vector<unsigned long long>(np, 0));
+    std::atomic<size_t> next{0};
+    auto mix = [](unsigned long long z) {
+      z += 0x9e3779b97f4a7c15ull;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      return z ^ (z >> 31);
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (size_t j; (j = next.fetch_add(1)) < jobs.size();) {
+          const ClassWork& cw = *jobs[j].first;
+          const long long e = std::min(cw.n, jobs[j].second + 4096);
+          auto add = [&](int px, int py) {
+            const int rx = pm[px].ref, ry = pm[py].ref;
+            const int lo = std::min(rx, ry), hi = std::max(rx, ry);
+            ++tc[t][lo];
+            th[t][lo] += mix(static_cast<unsigned long long>(hi));
+          };
+          for (long long k = jobs[j].second; k < e; ++k) {
+            const WorkItem& it = local_item(cw, k);
+            const int nq = it.r0nq >> 24;
+            int q = it.r0nq & 0xffffff, x = it.bra0, c = it.cntp;
+            for (int l = 0; l < nq; ++l, ++q) {
+              while (q >= cnt[c]) {
+                q -= cnt[c];
+                ++x;
+                ++c;
+              }
+              const int y = it.yfirst + q;
+              if (!cw.fam) {
+                add(x, y);
+                continue;
+              }
+              const UnitMeta& a = um[x];
+              const UnitMeta& b = um[y];
+              for (int m = 0; m < a.nm; ++m)
+                for (int n = 0; n < b.nm; ++n) {
+                  if (x == y && m > n) continue;
+                  const int px = m ? a.m1 : a.m0, py = n ? b.m1 : b.m0;
+                  if (tau > 0.0 && Q[px] * Q[py] < tau) continue;
+                  add(px, py);
+                }
+            }
+          }
+        }
+      });
+    for (auto& t : pool) t.join();
+    long long total = 0;
+    for (size_t x = 0; x < np; ++x) {
+      long long cx = 0;
+      unsigned long long hx = 0;
+      for (unsigned t = 0; t < nt; ++t) {
+        cx += tc[t][x];
+        hx += th[t][x];
+      }
+      count[x] = cx;
+      ysum[x] = hx;
+      total += cx;
+    }
+    return total;
+  }
+
   void check_ready() {
     if (host_only) throw CudaError("build_jk needs a CUDA device (host-only context)");
     if (!have_lists) throw StateError("build_jk before set_screening");
+    ensure_dealt();
+  }
+  // item k of this rank's share of class list cw
+  const WorkItem& local_item(const ClassWork& cw, long long k) const {
+    return nranks == 1 ? all_items[cw.aoff + k] : items[cw.off + k];
   }
 };
 
@@ -1050,7 +1259,7 @@ int eritile_gpu_create(int device, eritile_gpu** out) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
-    c->d_boys.upload(make_boys_table());
+    c->d_boys.upload(make_boys_table(), c->stream);
   });
   if (rc != ERITILE_OK) {
     g_create_err = c->err;
@@ -1162,7 +1371,7 @@ int eritile_gpu_set_shard(eritile_gpu* ctx, int rank, int nranks) {
   if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, ERITILE_ERR_ARG, "bad shard");
   ctx->rank = rank;
   ctx->nranks = nranks;
-  ctx->have_lists = false;
+  ctx->dealt = false;  // re-dealt before the next build / list export
   return ERITILE_OK;
 }
 
@@ -1171,15 +1380,22 @@ int eritile_gpu_set_screening(eritile_gpu* ctx, double tau) {
   return guard(ctx, [&] { ctx->set_screening(tau); });
 }
 
-long long eritile_gpu_num_quartets(const eritile_gpu* ctx) { return ctx ? ctx->quartets : -1; }
+long long eritile_gpu_num_quartets(const eritile_gpu* ctx) {
+  if (!ctx) return -1;
+  if (guard(const_cast<eritile_gpu*>(ctx), [&] { const_cast<eritile_gpu*>(ctx)->ensure_dealt(); }) != ERITILE_OK)
+    return -1;
+  return ctx->quartets;
+}
 
 long long eritile_gpu_quartets(const eritile_gpu* ctx, int* xs, int* ys, long long cap) {
   if (!ctx || !ctx->have_lists) return -1;
+  if (guard(const_cast<eritile_gpu*>(ctx), [&] { const_cast<eritile_gpu*>(ctx)->ensure_dealt(); }) != ERITILE_OK)
+    return -1;
   std::vector<std::pair<int, int>> q;
   q.reserve(static_cast<size_t>(ctx->quartets));
   for (const ClassWork& cw : ctx->work)
-    for (long long w = cw.off; w < (ctx->active(cw) ? cw.off + cw.n : cw.off); ++w) {
-      const WorkItem& it = ctx->items[w];
+    for (long long w = 0; w < (ctx->active(cw) ? cw.n : 0); ++w) {
+      const WorkItem& it = ctx->local_item(cw, w);
       const int nq = it.r0nq >> 24;
       for (int l = 0; l < nq; ++l) {
         int qq = (it.r0nq & 0xffffff) + l, x = it.bra0, c = it.cntp;
@@ -1291,12 +1507,12 @@ int eritile_gpu_boys(eritile_gpu* ctx, int m_max, const double* T, int n, double
       return fail(ctx, ERITILE_ERR_DOMAIN, "boys: argument must be finite and non-negative");
   return guard(ctx, [&] {
     DevBuf<double> dT, dF;
-    dT.upload(std::vector<double>(T, T + n));
+    dT.upload(std::vector<double>(T, T + n), ctx->stream);
     dF.alloc(static_cast<size_t>(n) * (m_max + 1) + 1);
     k_boys<<<(n + 127) / 128 + 1, 128, 0, ctx->stream>>>(m_max, dT.p, n, ctx->d_boys.p, dF.p);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaMemcpy(F, dF.p, sizeof(double) * n * (m_max + 1), cudaMemcpyDeviceToHost));
+    dF.download(F, static_cast<size_t>(n) * (m_max + 1), ctx->stream);
   });
 }
 
@@ -1324,7 +1540,7 @@ int eritile_gpu_eri_quartet(eritile_gpu* ctx, int x, int y, double* out) {
     for (int s = 0; s < 4; ++s) nslot[s] = (L[s] + 1) * (L[s] + 2) / 2;
     const int nv = nslot[0] * nslot[1] * nslot[2] * nslot[3];
     DevBuf<int> dq;
-    dq.upload(std::vector<int>{pb, pk});
+    dq.upload(std::vector<int>{pb, pk}, ctx->stream);
     DevBuf<double> dv;
     dv.alloc(nv);
     LaunchArgs a{};
@@ -1341,7 +1557,7 @@ int eritile_gpu_eri_quartet(eritile_gpu* ctx, int x, int y, double* out) {
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     std::vector<double> v(nv);
-    CK(cudaMemcpy(v.data(), dv.p, sizeof(double) * nv, cudaMemcpyDeviceToHost));
+    dv.download(v.data(), nv, ctx->stream);
     // reference positions (i, j | k, l) -> kernel slots
     const int R[4] = {ctx->ref_i[x], ctx->ref_j[x], ctx->ref_i[y], ctx->ref_j[y]};
     int slot_of[4];
@@ -1382,7 +1598,10 @@ int eritile_gpu_set_profiling(eritile_gpu* ctx, int on) {
 int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, double* flops,
                               long long* quartets, long long* prim_quartets) {
   if (!ctx) return ERITILE_ERR_ARG;
-  int rc = guard(ctx, [&] { ctx->collect_profile(); });
+  int rc = guard(ctx, [&] {
+    ctx->ensure_dealt();
+    ctx->collect_profile();
+  });
   if (rc != ERITILE_OK) return rc;
   const std::vector<int> act = ctx->active_work();
   const int n = static_cast<int>(act.size());
@@ -1402,18 +1621,58 @@ int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, 
 
 int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out) {
   if (!ctx || !out) return ERITILE_ERR_ARG;
+  const int rc = guard(const_cast<eritile_gpu*>(ctx), [&] { const_cast<eritile_gpu*>(ctx)->ensure_dealt(); });
+  if (rc != ERITILE_OK) return rc;
   out->nbf = ctx->nbf;
   out->nshells = static_cast<int>(ctx->shells.size());
   out->npairs = static_cast<int>(ctx->pm.size());
   out->nclasses = static_cast<int>(ctx->active_work().size());
   out->quartets = ctx->quartets;
   out->prim_quartets = ctx->prim_quartets;
-  out->work_items = static_cast<long long>(ctx->items.size());
+  out->work_items = 0;
+  for (const ClassWork& cw : ctx->work)
+    if (ctx->active(cw)) out->work_items += cw.n;
   out->model_flops = ctx->model_flops;
   out->last_build_ms = ctx->last_build_ms;
   out->last_schwarz_ms = ctx->last_schwarz_ms;
   out->gpu_launches_last_build = ctx->launches_last;
+  out->job_quartets = out->job_prim_quartets = out->pair_path_prim_quartets = 0;
+  out->job_model_flops = out->pair_path_model_flops = 0.0;
+  for (const ClassWork& cw : ctx->work) {
+    if (ctx->active(cw)) {
+      out->job_quartets += cw.aquartets;
+      out->job_prim_quartets += cw.aprim;
+      out->job_model_flops += cw.full_flops();
+    }
+    if (!cw.fam) {
+      out->pair_path_prim_quartets += cw.aprim;
+      out->pair_path_model_flops += cw.full_flops();
+    }
+  }
   return ERITILE_OK;
+}
+
+int eritile_gpu_get_variants(const eritile_gpu* ctx, int* var, int cap) {
+  if (!ctx || (cap > 0 && !var)) return ERITILE_ERR_ARG;
+  for (int c = 0; c < std::min(cap, kNumClasses); ++c) var[c] = ctx->variant(c);
+  return kNumClasses;
+}
+
+int eritile_gpu_set_variants(eritile_gpu* ctx, const int* var, int n) {
+  if (!ctx || !var || n != kNumClasses) return fail(ctx, ERITILE_ERR_ARG, "set_variants: one entry per class");
+  for (int c = 0; c < n; ++c)
+    if (var[c] < ctx->var_lo(c) || var[c] >= ctx->var_hi(c))
+      return fail(ctx, ERITILE_ERR_ARG, "set_variants: variant not available for class " + std::to_string(c));
+  ctx->var_choice.assign(var, var + n);
+  ctx->dealt = false;
+  return ERITILE_OK;
+}
+
+long long eritile_gpu_pair_survivors(const eritile_gpu* ctx, long long* count, unsigned long long* ysum) {
+  if (!ctx || !ctx->have_lists || !count || !ysum) return -1;
+  eritile_gpu* c = const_cast<eritile_gpu*>(ctx);
+  if (guard(c, [&] { c->ensure_dealt(); }) != ERITILE_OK) return -1;
+  return c->pair_survivors(count, ysum);
 }
 
 int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps) {
@@ -1423,7 +1682,7 @@ int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps) {
     ctx->ensure_mats();
     const size_t NN = static_cast<size_t>(ctx->nbf) * ctx->nbf;
     ctx->d_D.alloc(NN);
-    CK(cudaMemcpy(ctx->d_D.p, D, sizeof(double) * NN, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(ctx->d_D.p, D, sizeof(double) * NN, cudaMemcpyHostToDevice, ctx->stream));
     ctx->prescale(ctx->d_D.p, ctx->d_Ds.p, ctx->stream);
     ctx->tune(ctx->d_Ds.p, reps);
   });
@@ -1455,7 +1714,7 @@ int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var) {
     return fail(ctx, ERITILE_ERR_ARG, "kernel variant not available (families on: fam_* only)");
   if (ctx->var_choice.empty()) ctx->var_choice.assign(kNumClasses, -1);
   ctx->var_choice[cls_index] = var;
-  ctx->update_totals();
+  ctx->dealt = false;  // the active lists (pair / unit) may change: re-deal
   return ERITILE_OK;
 }
 

@@ -253,16 +253,9 @@ void launch_coop(const CoopTables& tb, const LaunchArgs& a) {
   const size_t smem = CoopSmem<C>::bytes(tb.nslots);
   const long long n = a.mode == 0 ? a.nitems : (a.mode == 1 ? a.npair_list : a.nq);
   if (n <= 0) return;
-  static int blocks_per_sm = 0, sms = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(coop_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, coop_kernel<C>, C::NT, smem);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  const long long cap = static_cast<long long>(blocks_per_sm) * sms;
+  const LaunchSetup ls = launch_setup(reinterpret_cast<const void*>(coop_kernel<C>), C::NT, smem, false);
+  if (!ls.bps) return;  // CUDA error pending for the caller's check
+  const long long cap = static_cast<long long>(ls.bps) * ls.sms;
   const int grid = a.grid > 0 ? a.grid : static_cast<int>(n < cap ? n : cap);
   coop_kernel<C><<<grid, C::NT, smem, a.stream>>>(tb, a);
 }
@@ -517,16 +510,10 @@ void launch_coopw(const CoopTables& tb, const LaunchArgs& a) {
   const size_t smem = sizeof(double) * kCoopWarps * (kCoopBase + kCoopMaxCombo + tb.nslots + DBLK);
   const long long n = a.mode == 0 ? a.nitems : (a.mode == 1 ? a.npair_list : a.nq);
   if (n <= 0) return;
-  static int blocks_per_sm = 0, sms = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(coopw_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, coopw_kernel<C>, 32 * kCoopWarps, smem);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  const long long cap = static_cast<long long>(blocks_per_sm) * sms;
+  const LaunchSetup ls =
+      launch_setup(reinterpret_cast<const void*>(coopw_kernel<C>), 32 * kCoopWarps, smem, false);
+  if (!ls.bps) return;  // CUDA error pending for the caller's check
+  const long long cap = static_cast<long long>(ls.bps) * ls.sms;
   const long long want = (n + kCoopWarps - 1) / kCoopWarps;
   const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
   coopw_kernel<C><<<grid, 32 * kCoopWarps, smem, a.stream>>>(tb, a);

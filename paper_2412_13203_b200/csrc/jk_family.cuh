@@ -248,20 +248,11 @@ void launch_fam_seg(const LaunchArgs& a, long long i0, long long i1) {
   if (i1 <= i0) return;
   const size_t smem =
       BoysStage<C>::bytes + (STYLE == kLoopSmemBra ? (sizeof(PrimRec) + sizeof(double2)) * kSmemBraMax * (NT / 32) : 0);
-  static int blocks_per_sm = 0, sms = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>, NT,
-                                                  smem);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-    set_min_carveout(reinterpret_cast<const void*>(jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>), blocks_per_sm, smem);
-  }
+  const LaunchSetup ls =
+      launch_setup(reinterpret_cast<const void*>(jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>), NT, smem, true);
+  if (!ls.bps) return;  // CUDA error pending for the caller's check
   const long long want = (i1 - i0 + (NT / 32) - 1) / (NT / 32);
-  const long long cap = static_cast<long long>(blocks_per_sm) * sms;
+  const long long cap = static_cast<long long>(ls.bps) * ls.sms;
   const int grid = static_cast<int>(want < cap ? want : cap);
   jk_fam_kernel<C, MB, MK, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a, i0, i1);
 }

@@ -17,6 +17,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "jk_api.h"
 
 namespace eritile_b200 {
@@ -313,14 +317,44 @@ constexpr int kJkThreads = 256;
 
 // Shared-memory carveout just large enough for the resident CTAs, so the
 // rest of the SM's 256 KB L1/shared array caches primitive records.
-inline void set_min_carveout(const void* fn, int blocks_per_sm, size_t smem) {
+inline cudaError_t set_min_carveout(const void* fn, int blocks_per_sm, size_t smem) {
   const size_t need = static_cast<size_t>(blocks_per_sm) * (smem + 1024);
   int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024));
   pct = pct < 1 ? 1 : (pct > 100 ? 100 : pct);
-  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
-template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads, int KR = 0>
+// Per-(kernel, device) launch setup, done once per device: the dynamic
+// shared-memory opt-in (> 48 KB for the Boys slice), the residency query and
+// optionally the minimal carveout. Function attributes are per device, so a
+// second device in the same process gets its own setup. On a CUDA error the
+// result is {0, 0}, nothing is cached and the error stays pending for the
+// caller's cudaGetLastError() check.
+struct LaunchSetup {
+  int bps;  // resident CTAs per SM
+  int sms;
+};
+inline LaunchSetup launch_setup(const void* fn, int nt, size_t smem, bool min_carveout) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, LaunchSetup> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return {0, 0};
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(fn, dev, smem);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  LaunchSetup s{0, 0};
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.bps, fn, nt, smem) != cudaSuccess ||
+      cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return {0, 0};
+  if (s.bps < 1) s.bps = 1;
+  if (min_carveout && set_min_carveout(fn, s.bps, smem) != cudaSuccess) return {0, 0};
+  cache.emplace(key, s);
+  return s;
+}
+
+template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
 __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
                                                        const PairMeta* __restrict__ pm,
@@ -339,18 +373,6 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
   (void)staged;
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   const size_t nK = static_cast<size_t>(N);
-  // KR: rows bfa.. (NA) and bfb.. (NB) of K for the chunk's leading bra are
-  // accumulated in shared memory (kbuf) and flushed once per chunk
-  double* kbuf = s_boys + BoysStage<C>::nsl * kBoysRows * kBoysCols;
-  int xcur = -1;
-  auto kadd_a = [&](int x, int a, size_t col, double v, int bfa) {
-    if (KR && x == xcur) atomicAdd(kbuf + static_cast<size_t>(a) * nK + col, v);
-    else red_add(K + (bfa + a) * nK + col, v);
-  };
-  auto kadd_b = [&](int x, int b, size_t col, double v, int bfb) {
-    if (KR && x == xcur) atomicAdd(kbuf + static_cast<size_t>(C::NA + b) * nK + col, v);
-    else red_add(K + (bfb + b) * nK + col, v);
-  };
   auto process = [&](const WorkItem& it) {
     const int nq = it.r0nq >> 24;
     const bool active = lane < nq;
@@ -464,7 +486,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbd + b * n + d), s);
-          kadd_a(x, a, km.bfa + c2, s * wk, bm.bfa);
+          red_add(K + (bm.bfa + a) * n + km.bfa + c2, s * wk);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
@@ -476,7 +498,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int c2 = 0; c2 < C::NC; ++c2)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dac + a * n + c2), s);
-          kadd_b(x, b, km.bfb + d, s * wk, bm.bfb);
+          red_add(K + (bm.bfb + b) * n + km.bfb + d, s * wk);
         }
       // K_ad += sum_bc v D_bc ; K_bc += sum_ad v D_ad
 #pragma unroll
@@ -489,7 +511,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int c2 = 0; c2 < C::NC; ++c2)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbc + b * n + c2), s);
-          kadd_a(x, a, km.bfb + d, s * wk, bm.bfa);
+          red_add(K + (bm.bfa + a) * n + km.bfb + d, s * wk);
         }
 #pragma unroll
       for (int b = 0; b < C::NB; ++b)
@@ -501,41 +523,17 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
 #pragma unroll
             for (int d = 0; d < C::ND; ++d)
               s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dad + a * n + d), s);
-          kadd_b(x, b, km.bfa + c2, s * wk, bm.bfb);
+          red_add(K + (bm.bfb + b) * n + km.bfa + c2, s * wk);
         }
     }
   };
-  if constexpr (KR) {
-    constexpr int kRows = C::NA + C::NB;
-    constexpr long long kChunk = (NT / 32) * 8;  // items per CTA chunk
-    const long long nchunks = (nitems + kChunk - 1) / kChunk;
-    for (long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-      const long long w0 = ch * kChunk, w1 = (w0 + kChunk < nitems) ? w0 + kChunk : nitems;
-      xcur = items[w0].bra0;
-      const int bfa_cur = pm[xcur].bfa, bfb_cur = pm[xcur].bfb;
-      for (size_t e = threadIdx.x; e < kRows * nK; e += NT) kbuf[e] = 0.0;
-      __syncthreads();
-      for (long long w = w0 + (threadIdx.x >> 5); w < w1; w += NT / 32) process(items[w]);
-      __syncthreads();
-      for (size_t e = threadIdx.x; e < kRows * nK; e += NT) {
-        const double v = kbuf[e];
-        if (v != 0.0) {
-          const int r = static_cast<int>(e / nK);
-          const size_t col = e % nK;
-          red_add(K + (r < C::NA ? bfa_cur + r : bfb_cur + (r - C::NA)) * nK + col, v);
-        }
-      }
-      __syncthreads();
-    }
-  } else {
-    long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    WorkItem nxt = w < nitems ? items[w] : WorkItem{};
-    for (; w < nitems; w += warps) {
-      // the next task's descriptor is fetched one task ahead (hides its L2 trip)
-      const WorkItem it = nxt;
-      if (w + warps < nitems) nxt = items[w + warps];
-      process(it);
-    }
+  long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  WorkItem nxt = w < nitems ? items[w] : WorkItem{};
+  for (; w < nitems; w += warps) {
+    // the next task's descriptor is fetched one task ahead (hides its L2 trip)
+    const WorkItem it = nxt;
+    if (w + warps < nitems) nxt = items[w + warps];
+    process(it);
   }
 }
 
@@ -594,50 +592,17 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 // NT: threads per CTA. One Boys slice is staged per CTA, so 512/768-thread
 // CTAs at MINB = 1 keep 16/24 warps per SM with a single 51 KB table and
 // leave the rest of the 256 KB L1/shared array to L1 (primitive records).
-// KR = 1: K rows of each chunk's leading bra accumulated in shared memory
-// ((NA + NB) x N doubles); when they do not fit, the KR = 0 kernel runs.
-// Measured 3-30% slower than the RED.ADD.F64 path on (H2O)_80 (shared FP64
-// atomics are CAS loops on sm_100a), so no registry variant uses it; kept
-// as the allocator's hook for systems with heavier K-row reuse.
-template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads, int KR = 0>
+template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
 void launch_class(const LaunchArgs& a) {
-  if constexpr (KR) {
-    if (a.mode != 0) return launch_class<C, MINB, STYLE, NT, 0>(a);
-    if (a.nitems <= 0) return;
-    const size_t smem = BoysStage<C>::bytes + sizeof(double) * (C::NA + C::NB) * static_cast<size_t>(a.N);
-    if (smem > 220 * 1024) return launch_class<C, MINB, STYLE, NT, 0>(a);
-    cudaFuncSetAttribute(jk_kernel<C, MINB, STYLE, NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    int bps = 0, sms = 0, dev = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, jk_kernel<C, MINB, STYLE, NT, 1>, NT, smem);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (bps < 1) return launch_class<C, MINB, STYLE, NT, 0>(a);
-    const long long chunk = (NT / 32) * 8;
-    const long long want = (a.nitems + chunk - 1) / chunk;
-    const long long cap = static_cast<long long>(bps) * sms;
-    const int grid = static_cast<int>(want < cap ? want : cap);
-    jk_kernel<C, MINB, STYLE, NT, 1><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D,
-                                                                  a.J, a.K, a.N, a.boys_tab, a.kprims);
-    return;
-  }
   const size_t smem = BoysStage<C>::bytes +
                       (STYLE == kLoopSmemBra && a.mode == 0 ? sizeof(PrimRec) * kSmemBraMax * (NT / 32) : 0);
   if (a.mode == 0) {
     if (a.nitems <= 0) return;
-    static int blocks_per_sm = 0;
-    static int sms = 0;
-    if (!blocks_per_sm) {
-      cudaFuncSetAttribute(jk_kernel<C, MINB, STYLE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, jk_kernel<C, MINB, STYLE, NT>, NT, smem);
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (blocks_per_sm < 1) blocks_per_sm = 1;
-      set_min_carveout(reinterpret_cast<const void*>(jk_kernel<C, MINB, STYLE, NT>), blocks_per_sm, smem);
-    }
+    const LaunchSetup ls =
+        launch_setup(reinterpret_cast<const void*>(jk_kernel<C, MINB, STYLE, NT>), NT, smem, true);
+    if (!ls.bps) return;  // CUDA error pending for the caller's check
     const long long want = (a.nitems + (NT / 32) - 1) / (NT / 32);
-    const long long cap = static_cast<long long>(blocks_per_sm) * sms;
+    const long long cap = static_cast<long long>(ls.bps) * ls.sms;
     const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
     jk_kernel<C, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
                                                        a.K, a.N, a.boys_tab, a.kprims);

@@ -36,7 +36,10 @@ class Stats(C.Structure):
                 ("quartets", C.c_longlong), ("prim_quartets", C.c_longlong),
                 ("work_items", C.c_longlong), ("model_flops", C.c_double),
                 ("last_build_ms", C.c_double), ("last_schwarz_ms", C.c_double),
-                ("gpu_launches_last_build", C.c_int)]
+                ("gpu_launches_last_build", C.c_int),
+                ("job_quartets", C.c_longlong), ("job_prim_quartets", C.c_longlong),
+                ("job_model_flops", C.c_double),
+                ("pair_path_prim_quartets", C.c_longlong), ("pair_path_model_flops", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -67,6 +70,9 @@ def _lib():
         "eritile_gpu_set_screening": (C.c_int, [C.c_void_p, C.c_double]),
         "eritile_gpu_num_quartets": (C.c_longlong, [C.c_void_p]),
         "eritile_gpu_quartets": (C.c_longlong, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong]),
+        "eritile_gpu_pair_survivors": (C.c_longlong, [C.c_void_p, C.c_void_p, C.c_void_p]),
+        "eritile_gpu_get_variants": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+        "eritile_gpu_set_variants": (C.c_int, [C.c_void_p, _ip, C.c_int]),
         "eritile_gpu_build_jk": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
         "eritile_gpu_build_jk_partial_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
         "eritile_gpu_finalize_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -216,6 +222,29 @@ class Engine:
         xs, ys = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.int32)
         self._lib.eritile_gpu_quartets(self._h, xs.ctypes.data, ys.ctypes.data, n)
         return xs[:n], ys[:n]
+
+    def pair_survivors(self):
+        """(count, ysum, total): per reference pair x, this rank's canonical
+        quartets (x, y >= x) and the wrapping sum of splitmix64(y) over them."""
+        n = self.npairs
+        cnt = np.zeros(n, np.int64)
+        ysum = np.zeros(n, np.uint64)
+        tot = self._lib.eritile_gpu_pair_survivors(self._h, cnt.ctypes.data, ysum.ctypes.data)
+        if tot < 0:
+            raise RuntimeError("pair_survivors before set_screening")
+        return cnt, ysum, int(tot)
+
+    def get_variants(self) -> np.ndarray:
+        """The whole variant table (one index per class)."""
+        n = self._lib.eritile_gpu_get_variants(self._h, None, 0)
+        v = np.zeros(n, np.int32)
+        self._lib.eritile_gpu_get_variants(self._h, v.ctypes.data, n)
+        return v
+
+    def set_variants(self, var) -> "Engine":
+        v = np.ascontiguousarray(var, dtype=np.int32)
+        self._check(self._lib.eritile_gpu_set_variants(self._h, v, len(v)))
+        return self
 
     # -- executor (SPEC.md:325-343)
     def build_jk(self, D: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:

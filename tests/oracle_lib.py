@@ -75,7 +75,11 @@ class Oracle:
                                         C.c_longlong, _dp, _dp, C.POINTER(C.c_longlong)])
         f("build_jk_timed", C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_longlong, C.c_longlong,
                                        _dp, _dp, C.POINTER(C.c_longlong), C.POINTER(C.c_double)])
+        f("pair_survivors", C.c_longlong, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p])
         if kind == "orc":
+            f("build_jk_dsparse", C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, _dp, _dp,
+                                            C.POINTER(C.c_longlong)])
+            f("build_jk_list", C.c_int, [C.c_void_p, _dp, C.c_longlong, _ip, _ip, C.c_int, _dp, _dp])
             f("one_electron", C.c_int, [C.c_void_p, _dp, _dp, _dp])
             f("nuclear_repulsion", C.c_double, [C.c_void_p])
         else:
@@ -181,6 +185,38 @@ class System:
         if rc != 0:
             raise RuntimeError(self.o._last_error().decode())
         return J, K, nq.value
+
+    def build_jk_dsparse(self, D: np.ndarray, tau: float = 0.0, nthreads: int = 0):
+        """True J, K for a density with zero shell blocks: quartets whose six D
+        blocks are all zero are skipped (exactly zero contributions)."""
+        N = self.nbf
+        D = np.ascontiguousarray(D, dtype=np.float64)
+        J, K = np.zeros((N, N)), np.zeros((N, N))
+        nq = C.c_longlong(0)
+        if self.o._build_jk_dsparse(self.h, D, tau, nthreads, J, K, C.byref(nq)) != 0:
+            raise RuntimeError(self.o._last_error().decode())
+        return J, K, nq.value
+
+    def build_jk_list(self, D: np.ndarray, xs, ys, nthreads: int = 0):
+        """True-J/K convention partial sums over an explicit canonical quartet
+        list (x <= y): summing the results of a disjoint cover gives build_jk."""
+        N = self.nbf
+        D = np.ascontiguousarray(D, dtype=np.float64)
+        xs = np.ascontiguousarray(xs, dtype=np.int32)
+        ys = np.ascontiguousarray(ys, dtype=np.int32)
+        J, K = np.zeros((N, N)), np.zeros((N, N))
+        if self.o._build_jk_list(self.h, D, len(xs), xs, ys, nthreads, J, K) != 0:
+            raise RuntimeError(self.o._last_error().decode())
+        return J, K
+
+    def pair_survivors(self, tau: float):
+        """(count, ysum, total) per pair x over canonical survivors (x, y >= x)."""
+        cnt = np.zeros(self.npairs, np.int64)
+        ys = np.zeros(self.npairs, np.uint64)
+        tot = self.o._pair_survivors(self.h, tau, cnt.ctypes.data, ys.ctypes.data)
+        if tot < 0:
+            raise RuntimeError(self.o._last_error().decode())
+        return cnt, ys, int(tot)
 
     def build_jk_timed(self, D: np.ndarray, tau: float, nthreads: int, stride: int, offset: int):
         """(J, K, quartets, seconds of the parallel ERI+digestion phase)."""
