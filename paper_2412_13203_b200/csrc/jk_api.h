@@ -50,6 +50,18 @@ struct alignas(16) UnitMeta {
   double ABx, ABy, ABz, pad3;
 };
 
+// A strip (csrc/jk_strip.cuh): the single-bra items [i0, i1) of one bra pair
+// (or bra unit) run by one CTA that keeps the bra's K rows (and D rows) in
+// shared memory. Row blocks: the distinct shells of the bra members, in
+// shared-memory row order (rb_n = 0 unused); rowA/rowB: shared-memory row of
+// member m's first A / B component.
+struct alignas(16) Strip {
+  int bra, i0, i1, nrows;
+  int rowA[2], rowB[2];
+  int rb_bf[4];
+  int rb_n[4];
+};
+
 struct LaunchArgs {
   int mode;  // 0 = J/K digestion, 1 = Schwarz diagonal, 2 = raw quartets
   const WorkItem* items;
@@ -80,6 +92,15 @@ struct LaunchArgs {
   const double* Qp;      // Schwarz Q per product pair
   double tau;            // screening threshold (<= 0: none)
   long long seg[5];      // unit launches: item offsets of the (1,1) (1,2) (2,1) (2,2) member segments
+  // strip variants: per member segment sg, strips[sseg[sg] .. sseg[sg+1]) own
+  // the items [seg[sg], sitem[sg]); items [sitem[sg], seg[sg+1]) are packed
+  // multi-bra items for the lane kernels (pair lists: segment 0 only)
+  const Strip* strips;
+  long long sseg[5];
+  long long sitem[4];
+  const int* cols;  // compact K/D column list of the class: L_C functions (++ L_D functions if L_D != L_C)
+  const int* cpos;  // per shell: first compact column within its own L list
+  int ncols, ncolC;
 };
 
 using LaunchFn = void (*)(const LaunchArgs&);

@@ -1,0 +1,332 @@
+// Bra-stationary strip kernels: on-chip J/K partial sums before global
+// atomics (north_star (3); SURVEY.md §7 "Digestion").
+//
+// Every K update of a canonical quartet (ab|cd) lands in a row of the BRA:
+//   K_ac += D_bd v, K_ad += D_bc v  (rows a)   K_bc += D_ad v, K_bd += D_ac v  (rows b)
+// (the K_bd / K_bc blocks are written with the bra index as row,
+// the finalize kernel symmetrises). The surviving kets of one bra are a long
+// Q-sorted run (thousands of quartets at N = 2000), so a CTA that owns one bra
+// pair (or bra unit) for a strip of its items keeps that bra's K rows in
+// shared memory, restricted to the columns of the class's ket shells (the
+// functions of shells with L = L_C, and L = L_D: 560 of 2000 columns for an
+// s-shell ket at (H2O)_80), reads the matching D rows from shared memory, and
+// accumulates J_ab in registers. Global traffic per quartet is then the J_cd
+// block (one RED per component) and the ket data; the K rows are flushed once
+// per strip (only non-zero entries). Shared FP64 adds are CAS loops on sm_100a
+// (ATOMS.CAST.SPIN.64), but conflict-free in the common case and far cheaper
+// than L2 RED.ADD.F64 on scattered addresses (211 G/s, profiles/r01_fp64_peak.json).
+//
+// Items of a strip are single-bra WorkItems (32 consecutive kets of one ket
+// group); warps of the CTA take them round-robin. The bra's primitive records
+// (and unit weights) are staged in shared memory once per strip; inner loops
+// read them as warp-broadcast LDS (kLoopSmemBra). Integrals and degeneracy are
+// exactly the lane kernel's (same generated prim()/finish(), same weights), so
+// results differ from the other variants only by summation order.
+#pragma once
+#include "jk_family.cuh"
+
+namespace eritile_b200 {
+
+// Shared memory of a strip kernel: Boys slice(s), bra records and weights,
+// the K rows and (DSM) the D rows, each MB * (NA + NB) rows x ncols.
+template <class C, int MB>
+struct StripSmem {
+  static constexpr int kRowsMax = MB * (C::NA + C::NB);
+  static size_t bytes(int ncols, bool dsm) {
+    return BoysStage<C>::bytes + (sizeof(PrimRec) + sizeof(double2)) * kSmemBraMax +
+           sizeof(double) * static_cast<size_t>(kRowsMax) * ncols * (dsm ? 2 : 1);
+  }
+};
+
+template <class C, bool FAM, int MB, int MK, int NT, bool DSM>
+__global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long s0, long long s1) {
+  extern __shared__ __align__(16) double smem[];
+  load_boys_for<C>(smem, a.boys_tab);
+  constexpr int kBoysD = BoysStage<C>::nsl * kBoysRows * kBoysCols;
+  PrimRec* sbra = reinterpret_cast<PrimRec*>(smem + kBoysD);
+  double2* sbw = reinterpret_cast<double2*>(sbra + kSmemBraMax);
+  double* sK = reinterpret_cast<double*>(sbw + kSmemBraMax);
+  const int ncol = a.ncols;
+  double* sD = sK + StripSmem<C, MB>::kRowsMax * ncol;
+  __shared__ int s_rowg[StripSmem<C, MB>::kRowsMax];  // global basis function of each smem row
+  (void)sD;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const size_t n = static_cast<size_t>(a.N);
+  constexpr int LDOFF = C::LC == C::LD ? 0 : 1;  // D-shell columns follow the C-shell list
+  for (long long s = s0 + blockIdx.x; s < s1; s += gridDim.x) {
+    const Strip st = a.strips[s];
+    const int nrows = st.nrows;
+    if (threadIdx.x < 4) {
+      int r = 0;
+      for (int k = 0; k < static_cast<int>(threadIdx.x); ++k) r += st.rb_n[k];
+      for (int t = 0; t < st.rb_n[threadIdx.x]; ++t) s_rowg[r + t] = st.rb_bf[threadIdx.x] + t;
+    }
+    // bra records (and unit weights): one copy per CTA for the whole strip
+    int kb, boff;
+    if constexpr (FAM) {
+      kb = a.um[st.bra].K;
+      boff = a.um[st.bra].prim_off;
+    } else {
+      kb = a.pm[st.bra].K;
+      boff = a.pm[st.bra].prim_off;
+    }
+    const bool bsm = kb <= kSmemBraMax;
+    if (bsm) {
+      const double2* src = reinterpret_cast<const double2*>(a.prims + boff);
+      double2* dst = reinterpret_cast<double2*>(sbra);
+      for (int t = threadIdx.x; t < kb * 5; t += NT) dst[t] = __ldg(src + t);
+      if constexpr (FAM)
+        for (int t = threadIdx.x; t < kb; t += NT) sbw[t] = __ldg(a.uw + boff + t);
+    }
+    for (int e = threadIdx.x; e < nrows * ncol; e += NT) sK[e] = 0.0;
+    __syncthreads();
+    if constexpr (DSM) {
+      for (int e = threadIdx.x; e < nrows * ncol; e += NT) {
+        const int r = e / ncol;
+        sD[e] = __ldg(a.D + static_cast<size_t>(s_rowg[r]) * n + __ldg(a.cols + (e - r * ncol)));
+      }
+      __syncthreads();
+    }
+    const PrimRec* brap = bsm ? sbra : a.prims + boff;
+    const double2* bwp = bsm ? sbw : a.uw + boff;
+    (void)bwp;
+    // J_ab partial sums, lane-private over all items of the strip
+    double jab[MB][C::NA * C::NB];
+#pragma unroll
+    for (int m = 0; m < MB; ++m)
+#pragma unroll
+      for (int e = 0; e < C::NA * C::NB; ++e) jab[m][e] = 0.0;
+    // bra members (pair strips: the pair itself)
+    int bpx[MB];
+    if constexpr (FAM) {
+      bpx[0] = a.um[st.bra].m0;
+      if constexpr (MB == 2) bpx[MB - 1] = a.um[st.bra].m1;
+    } else {
+      bpx[0] = st.bra;
+    }
+    for (long long w = st.i0 + warp; w < st.i1; w += NW) {
+      const WorkItem it = a.items[w];
+      const int nq = it.r0nq >> 24;
+      const bool active = lane < nq;
+      const int y = it.yfirst + (it.r0nq & 0xffffff) + (active ? lane : 0);  // single-bra item
+      double acc_v[MB][MK][C::NV];
+      (void)acc_v;
+      int kpy[MK];
+      double ABx, ABy, ABz, CDx, CDy, CDz;
+      if constexpr (FAM) {
+        const UnitMeta bu = a.um[st.bra];
+        const UnitMeta ku = a.um[y];
+        ABx = bu.ABx; ABy = bu.ABy; ABz = bu.ABz;
+        CDx = ku.ABx; CDy = ku.ABy; CDz = ku.ABz;
+        kpy[0] = ku.m0;
+        if constexpr (MK == 2) kpy[MK - 1] = ku.m1;
+        typename C::Acc acc[MB][MK];
+        fam_drive<C, MB, MK, kLoopSmemBra>(brap, bwp, kb, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, active ? ku.K : 0,
+                                           ku.kstride, smem, acc);
+#pragma unroll
+        for (int m = 0; m < MB; ++m)
+#pragma unroll
+          for (int k = 0; k < MK; ++k) C::finish(acc[m][k], ABx, ABy, ABz, CDx, CDy, CDz, acc_v[m][k]);
+      } else {
+        const PairMeta* bmp = a.pm + st.bra;
+        ABx = bmp->ABx; ABy = bmp->ABy; ABz = bmp->ABz;
+        const int4 kh = __ldg(reinterpret_cast<const int4*>(a.pm + y));
+        const double2 cd = __ldg(reinterpret_cast<const double2*>(&a.pm[y].ABx));
+        CDx = cd.x; CDy = cd.y; CDz = __ldg(&a.pm[y].ABz);
+        const int2 ks = __ldg(reinterpret_cast<const int2*>(&a.pm[y].ksoa));
+        const int kstride = __ldg(&a.pm[y].kstride);
+        kpy[0] = y;
+        eri_drive<C, kLoopSmemBra>(brap, kb, a.kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy,
+                                   CDz, smem, acc_v[0][0]);
+      }
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        PairMeta bm;
+        ld_meta_late(a.pm + bpx[m], bm);
+        const int rA = st.rowA[m], rB = st.rowB[m];
+#pragma unroll
+        for (int k = 0; k < MK; ++k) {
+          const int py = kpy[k];
+          bool keep = active;
+          if constexpr (FAM) {
+            keep = keep && !(st.bra == y && m > k) &&
+                   (a.tau <= 0.0 || __ldg(a.Qp + bpx[m]) * __ldg(a.Qp + py) >= a.tau);
+          }
+          if (!keep) continue;
+          PairMeta km;
+          ld_meta_late(a.pm + py, km);
+          const double* v = acc_v[m][k];
+          const double deg =
+              (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (bpx[m] != py ? 2.0 : 1.0);
+          const double wj = 0.5 * deg, wk = 0.25 * deg;
+          const int colC = __ldg(a.cpos + km.sha);
+          const int colD = __ldg(a.cpos + km.shb) + (LDOFF ? a.ncolC : 0);
+          const double* Dab = a.D + bm.bfa * n + bm.bfb;
+          const double* Dcd = a.D + km.bfa * n + km.bfb;
+          auto dsm = [&](int row, int col, size_t grow, size_t gcol) -> double {
+            if constexpr (DSM) return sD[row * ncol + col];
+            else return __ldg(a.D + grow * n + gcol);
+          };
+#pragma unroll
+          for (int ia = 0; ia < C::NA; ++ia)
+#pragma unroll
+            for (int ib = 0; ib < C::NB; ++ib) {
+              double t = 0.0;
+#pragma unroll
+              for (int ic = 0; ic < C::NC; ++ic)
+#pragma unroll
+                for (int id = 0; id < C::ND; ++id)
+                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dcd + ic * n + id), t);
+              jab[m][ia * C::NB + ib] = fma(t, wj, jab[m][ia * C::NB + ib]);
+            }
+#pragma unroll
+          for (int ic = 0; ic < C::NC; ++ic)
+#pragma unroll
+            for (int id = 0; id < C::ND; ++id) {
+              double t = 0.0;
+#pragma unroll
+              for (int ia = 0; ia < C::NA; ++ia)
+#pragma unroll
+                for (int ib = 0; ib < C::NB; ++ib)
+                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), t);
+              red_add(a.J + (km.bfa + ic) * n + km.bfb + id, t * wj);
+            }
+          // K_ac += sum_bd v D_bd ; K_ad += sum_bc v D_bc   (rows a of the bra)
+#pragma unroll
+          for (int ia = 0; ia < C::NA; ++ia) {
+#pragma unroll
+            for (int ic = 0; ic < C::NC; ++ic) {
+              double t = 0.0;
+#pragma unroll
+              for (int ib = 0; ib < C::NB; ++ib)
+#pragma unroll
+                for (int id = 0; id < C::ND; ++id)
+                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                          dsm(rB + ib, colD + id, bm.bfb + ib, km.bfb + id), t);
+              atomicAdd(sK + (rA + ia) * ncol + colC + ic, t * wk);
+            }
+#pragma unroll
+            for (int id = 0; id < C::ND; ++id) {
+              double t = 0.0;
+#pragma unroll
+              for (int ib = 0; ib < C::NB; ++ib)
+#pragma unroll
+                for (int ic = 0; ic < C::NC; ++ic)
+                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                          dsm(rB + ib, colC + ic, bm.bfb + ib, km.bfa + ic), t);
+              atomicAdd(sK + (rA + ia) * ncol + colD + id, t * wk);
+            }
+          }
+          // K_bd += sum_ac v D_ac ; K_bc += sum_ad v D_ad   (rows b of the bra)
+#pragma unroll
+          for (int ib = 0; ib < C::NB; ++ib) {
+#pragma unroll
+            for (int id = 0; id < C::ND; ++id) {
+              double t = 0.0;
+#pragma unroll
+              for (int ia = 0; ia < C::NA; ++ia)
+#pragma unroll
+                for (int ic = 0; ic < C::NC; ++ic)
+                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                          dsm(rA + ia, colC + ic, bm.bfa + ia, km.bfa + ic), t);
+              atomicAdd(sK + (rB + ib) * ncol + colD + id, t * wk);
+            }
+#pragma unroll
+            for (int ic = 0; ic < C::NC; ++ic) {
+              double t = 0.0;
+#pragma unroll
+              for (int ia = 0; ia < C::NA; ++ia)
+#pragma unroll
+                for (int id = 0; id < C::ND; ++id)
+                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                          dsm(rA + ia, colD + id, bm.bfa + ia, km.bfb + id), t);
+              atomicAdd(sK + (rB + ib) * ncol + colC + ic, t * wk);
+            }
+          }
+        }
+      }
+    }
+    // J_ab: one butterfly per strip and warp, one RED per element and warp
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      PairMeta bm;
+      ld_meta_late(a.pm + bpx[m], bm);
+#pragma unroll
+      for (int e = 0; e < C::NA * C::NB; ++e) {
+        double t = jab[m][e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0 && t != 0.0) red_add(a.J + (bm.bfa + e / C::NB) * n + bm.bfb + e % C::NB, t);
+      }
+    }
+    __syncthreads();
+    // flush the K rows (non-zero entries only)
+    for (int e = threadIdx.x; e < nrows * ncol; e += NT) {
+      const double v = sK[e];
+      if (v != 0.0) {
+        const int r = e / ncol;
+        red_add(a.K + static_cast<size_t>(s_rowg[r]) * n + __ldg(a.cols + (e - r * ncol)), v);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Strips of member segment (MB, MK) through the strip kernel; returns false
+// (nothing launched) if its shared memory does not fit - the caller then runs
+// those items through the lane kernel.
+template <class C, bool FAM, int MB, int MK, int NT>
+bool launch_strip_seg(const LaunchArgs& a, long long s0, long long s1) {
+  if (s1 <= s0) return true;
+  const size_t with_d = StripSmem<C, MB>::bytes(a.ncols, true);
+  const size_t no_d = StripSmem<C, MB>::bytes(a.ncols, false);
+  constexpr size_t kMax = 227 * 1024 - 1024;  // static s_rowg + reserve
+  if (no_d > kMax) return false;
+  const bool dsm = with_d <= kMax;
+  const void* fn = dsm ? reinterpret_cast<const void*>(jk_strip_kernel<C, FAM, MB, MK, NT, true>)
+                       : reinterpret_cast<const void*>(jk_strip_kernel<C, FAM, MB, MK, NT, false>);
+  const size_t smem = dsm ? with_d : no_d;
+  const LaunchSetup ls = launch_setup(fn, NT, smem, false);
+  if (!ls.bps) return true;  // CUDA error pending for the caller's check
+  const long long cap = static_cast<long long>(ls.bps) * ls.sms;
+  const int grid = static_cast<int>(s1 - s0 < cap ? s1 - s0 : cap);
+  if (dsm)
+    jk_strip_kernel<C, FAM, MB, MK, NT, true><<<grid, NT, smem, a.stream>>>(a, s0, s1);
+  else
+    jk_strip_kernel<C, FAM, MB, MK, NT, false><<<grid, NT, smem, a.stream>>>(a, s0, s1);
+  return true;
+}
+
+// Pair-list strip variant: strips through the strip kernel, the remaining
+// (multi-bra packed) items through the lane kernel <MINB, STYLE, NTL>.
+template <class C, int NT, int MINB, int STYLE, int NTL>
+void launch_strip(const LaunchArgs& a) {
+  if (a.mode != 0) return launch_class<C, 2, kLoopPrefetch>(a);
+  if (a.nitems <= 0) return;
+  LaunchArgs r = a;
+  if (launch_strip_seg<C, false, 1, 1, NT>(a, a.sseg[0], a.sseg[1])) {
+    r.items = a.items + a.sitem[0];
+    r.nitems = a.nitems - a.sitem[0];
+  }
+  launch_class<C, MINB, STYLE, NTL>(r);
+}
+
+// Unit-list strip variant: per member segment, strips through the strip
+// kernel and the rest through the unit lane kernel.
+template <class C, int NT, int MINB, int STYLE, int NTL, int NT11>
+void launch_fstrip(const LaunchArgs& a) {
+  if (a.mode != 0) return launch_class<C, 2, kLoopPrefetch>(a);
+  long long rest0[4];
+  for (int sg = 0; sg < 4; ++sg) rest0[sg] = a.seg[sg];
+  if (launch_strip_seg<C, true, 1, 1, NT>(a, a.sseg[0], a.sseg[1])) rest0[0] = a.sitem[0];
+  if (launch_strip_seg<C, true, 1, 2, NT>(a, a.sseg[1], a.sseg[2])) rest0[1] = a.sitem[1];
+  if (launch_strip_seg<C, true, 2, 1, NT>(a, a.sseg[2], a.sseg[3])) rest0[2] = a.sitem[2];
+  if (launch_strip_seg<C, true, 2, 2, NT>(a, a.sseg[3], a.sseg[4])) rest0[3] = a.sitem[3];
+  launch_fam_seg<C, 1, 1, MINB, STYLE, NT11>(a, rest0[0], a.seg[1]);
+  launch_fam_seg<C, 1, 2, MINB, STYLE, NTL>(a, rest0[1], a.seg[2]);
+  launch_fam_seg<C, 2, 1, MINB, STYLE, NTL>(a, rest0[2], a.seg[3]);
+  launch_fam_seg<C, 2, 2, MINB, STYLE, NTL>(a, rest0[3], a.seg[4]);
+}
+
+}  // namespace eritile_b200
