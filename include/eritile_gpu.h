@@ -170,6 +170,12 @@ int eritile_gpu_set_variants(eritile_gpu* ctx, const int* var, int n);
  * "fam_" variants then run only those. Takes effect at the next
  * set_screening. Results and quartet lists are unchanged. */
 int eritile_gpu_set_families(eritile_gpu* ctx, int on);
+/* Strip lists (bra-stationary CTAs, K rows in shared memory): bras with at
+ * least min_quartets survivors in a class get single-bra items grouped into
+ * strips of at most max_items warp tasks (defaults 1024, 256); the rest stay
+ * packed. Takes effect at the next set_screening; lists and results are
+ * unchanged, only the work layout. */
+int eritile_gpu_set_strips(eritile_gpu* ctx, long long min_quartets, int max_items);
 /* Class launches of a build on 4 streams (default) or on one stream. */
 int eritile_gpu_set_concurrent(eritile_gpu* ctx, int on);
 /* Active variant index range [lo, hi) of a class in this context. */

@@ -69,7 +69,8 @@ def build(jobs: int | None = None, verbose: bool = True) -> Path:
     OBJ.mkdir(exist_ok=True)
     LIBDIR.mkdir(exist_ok=True)
     generate()
-    kern_deps = [CSRC / "jk_kernels.cuh", CSRC / "jk_coop.cuh", CSRC / "jk_api.h"]
+    kern_deps = [CSRC / "jk_kernels.cuh", CSRC / "jk_coop.cuh", CSRC / "jk_family.cuh", CSRC / "jk_strip.cuh",
+                 CSRC / "jk_api.h"]
     host_deps = [CSRC / "host" / "molecule.h", CSRC / "host" / "onee.h", CSRC / "jk_api.h",
                  INCLUDE / "eritile_gpu.h"]
     units = []
@@ -78,7 +79,7 @@ def build(jobs: int | None = None, verbose: bool = True) -> Path:
     for src in gen:
         units.append((src, kern_deps, NVFLAGS, NVCC))
     units.append((GEN / "registry.cpp", [CSRC / "jk_api.h"], CXXFLAGS, "g++"))
-    units.append((CSRC / "host" / "engine.cu", host_deps, NVFLAGS, NVCC))
+    units.append((CSRC / "host" / "engine.cu", host_deps + kern_deps, NVFLAGS, NVCC))
     units.append((CSRC / "host" / "molecule.cpp", host_deps, CXXFLAGS, "g++"))
     units.append((CSRC / "host" / "onee.cpp", host_deps, CXXFLAGS, "g++"))
     jobs = jobs or max(2, os.cpu_count() or 2)

@@ -282,6 +282,10 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("lane_sb512", f"launch_class<Cls{cid}, 1, kLoopSmemBra, 512>"))
         if info["ops"] <= UNROLL2_MAX_OPS:
             out.append(("lane_u2t512", f"launch_class<Cls{cid}, 1, kLoopTwoKet, 512>"))
+        # bra-stationary strips (csrc/jk_strip.cuh): K rows in shared memory;
+        # the packed multi-bra remainder runs on a lane kernel
+        if info["ops"] <= MINB_SMALL_OPS:
+            out.append(("strip_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
         if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:
@@ -292,12 +296,19 @@ def variants(info) -> List[Tuple[str, str]]:
         out.append(("fam_pl512", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512>"))
         out.append(("fam_pl768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 768>"))
         out.append(("fam_x768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 768>"))
+        out.append(("fstrip_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768>"))
+        out.append(("fstrip_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768>"))
     assert len(out) <= 16, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 
 
+def is_unit_variant(name: str) -> bool:
+    """Variants that run the shared-primitive unit lists (kept last)."""
+    return name.startswith("fam_") or name.startswith("fstrip")
+
+
 def default_variant(info, vs) -> int:
-    names = [v[0] for v in vs if not v[0].startswith("fam_")]
+    names = [v[0] for v in vs if not is_unit_variant(v[0])]
     if "coop" in names and (info["ops"] >= 2000 or len(names) == 1):
         return names.index("coop")
     return 0
@@ -322,7 +333,7 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         lane = any(n.startswith("lane") for n, _ in vs)
         coop = any(n == "coop" for n, _ in vs)
         src = ["// GENERATED by paper_2412_13203_b200/compiler/emit_cuda.py — do not edit.",
-               '#include "../jk_coop.cuh"', '#include "../jk_family.cuh"', "namespace eritile_b200 {"]
+               '#include "../jk_coop.cuh"', '#include "../jk_strip.cuh"', "namespace eritile_b200 {"]
         if lane:
             src.append(body)
         else:  # sizes only; the straight-line body is not emitted
@@ -385,7 +396,7 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
         vs = info["variants"]
         fns = ", ".join(f"&{fn(n, cid)}" for n, _ in vs) + ", nullptr" * (16 - len(vs))
         names = ", ".join(f'"{n}"' for n, _ in vs) + ", nullptr" * (16 - len(vs))
-        nfam = sum(1 for n, _ in vs if n.startswith("fam_"))
+        nfam = sum(1 for n, _ in vs if is_unit_variant(n))
         fam_def = len(vs) - nfam if nfam else -1
         reg.append(f"  {{{la}, {lb}, {lc}, {ld}, {info['M']}, {info['ops']}, {info['prim_terms']}, "
                    f"{info['base']}, {info['contract']}, {info['hrr_terms']}, {len(vs)}, {{{fns}}}, "

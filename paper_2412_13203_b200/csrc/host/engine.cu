@@ -198,8 +198,17 @@ struct ClassWork {
   long long aseg[5] = {0, 0, 0, 0, 0};
   long long aquartets = 0, aprim = 0;
   double cost_prim = 0.0, cost_q = 0.0;  // model FLOPs per primitive / contracted quartet
+  // strips (csrc/jk_strip.cuh): per member segment sg, strips [asseg[sg],
+  // asseg[sg+1]) of all_strips (from astrip_off) own the single-bra items
+  // [aseg[sg], asitem[sg]); the packed multi-bra items follow up to aseg[sg+1]
+  long long astrip_off = 0;
+  long long asseg[5] = {0, 0, 0, 0, 0};
+  long long asitem[4] = {0, 0, 0, 0};
   long long off = 0, n = 0;
   long long seg[5] = {0, 0, 0, 0, 0};
+  long long strip_off = 0;
+  long long sseg[5] = {0, 0, 0, 0, 0};
+  long long sitem[4] = {0, 0, 0, 0};
   long long quartets = 0, prim_quartets = 0;
   double flops = 0.0;    // model FLOPs of this rank's launch
   double last_ms = 0.0;  // device time of the last launch (profiling mode)
@@ -241,6 +250,13 @@ struct eritile_gpu {
   std::vector<unsigned char> item_q;      // contracted quartets per item (all_items)
   std::vector<unsigned> item_p;           // primitive quartets per item (all_items)
   std::vector<WorkItem> items;            // this rank's items (nranks > 1)
+  std::vector<Strip> all_strips, strips;  // strip tables (full lists / this rank)
+  // compact K/D columns per ket class (L_C, L_D): list of the L_C functions
+  // (++ the L_D functions when L_D != L_C); cpos per shell
+  std::vector<int> shell_cpos, cols_all;
+  int cols_off[8][8] = {}, cols_n[8][8] = {}, cols_nc[8][8] = {};
+  DevBuf<int> d_cpos, d_cols;
+  DevBuf<Strip> d_all_strips, d_strips;
   std::vector<int> cnt;  // survivor counts per (group pair, bra) + sentinel
   std::vector<ClassWork> work;
   bool dealt = false;   // rank-local lists match the current variants and shard
@@ -413,6 +429,16 @@ struct eritile_gpu {
     a.stream = st;
     a.block = 128;
     for (int k = 0; k < 5; ++k) a.seg[k] = full ? cw.aseg[k] : cw.seg[k];
+    for (int k = 0; k < 5; ++k) a.sseg[k] = use_all ? cw.asseg[k] : cw.sseg[k];
+    for (int k = 0; k < 4; ++k) a.sitem[k] = use_all ? cw.asitem[k] : cw.sitem[k];
+    a.strips = use_all ? d_all_strips.p + cw.astrip_off : d_strips.p + cw.strip_off;
+    {
+      const ClassEntry& ce = kClassTable[cw.cls];
+      a.cols = d_cols.p + cols_off[ce.lc][ce.ld];
+      a.ncols = cols_n[ce.lc][ce.ld];
+      a.ncolC = cols_nc[ce.lc][ce.ld];
+      a.cpos = d_cpos.p;
+    }
     if (cw.fam) {
       a.um = d_um.p;
       a.uw = d_uw.p;
@@ -458,6 +484,29 @@ struct eritile_gpu {
         k.insert(k.end(), shells[i].exps.begin(), shells[i].exps.end());
         auto it = ids.emplace(k, static_cast<int>(ids.size())).first;
         sib[i] = it->second;
+      }
+    }
+    // compact columns for the strip kernels
+    {
+      std::vector<std::vector<int>> lists(kMaxL + 1);
+      shell_cpos.assign(shells.size(), 0);
+      for (size_t i = 0; i < shells.size(); ++i) {
+        const int L = shells[i].L;
+        shell_cpos[i] = static_cast<int>(lists[L].size());
+        for (int f = 0; f < shells[i].nfunc(); ++f) lists[L].push_back(bf_off[i] + f);
+      }
+      cols_all.clear();
+      for (int lc = 0; lc <= kMaxL; ++lc)
+        for (int ld = 0; ld <= kMaxL; ++ld) {
+          cols_off[lc][ld] = static_cast<int>(cols_all.size());
+          cols_all.insert(cols_all.end(), lists[lc].begin(), lists[lc].end());
+          if (ld != lc) cols_all.insert(cols_all.end(), lists[ld].begin(), lists[ld].end());
+          cols_nc[lc][ld] = static_cast<int>(lists[lc].size());
+          cols_n[lc][ld] = static_cast<int>(cols_all.size()) - cols_off[lc][ld];
+        }
+      if (!host_only) {
+        d_cpos.upload(shell_cpos, stream);
+        d_cols.upload(cols_all, stream);
       }
     }
     have_mol = true;
@@ -845,10 +894,13 @@ struct eritile_gpu {
     item_q.clear();
     item_p.clear();
     items.clear();
+    all_strips.clear();
+    strips.clear();
     work.clear();
     cnt.clear();
     quartets = prim_quartets = 0;
     model_flops = 0.0;
+    std::vector<long long> bra_tot;  // survivors per bra in the current (class, list, segment)
     for (size_t s = 0; s < gps.size();) {
       const int cls = gps[s].cls;
       const bool fam = gps[s].fam;
@@ -856,51 +908,53 @@ struct eritile_gpu {
       cw.cls = cls;
       cw.fam = fam;
       cw.aoff = static_cast<long long>(all_items.size());
-      int cur_seg = 0;
-      for (; s < gps.size() && gps[s].cls == cls && gps[s].fam == fam; ++s) {
-        while (cur_seg < gps[s].seg) cw.aseg[++cur_seg] = static_cast<long long>(all_items.size()) - cw.aoff;
-        const Group& gx = fam ? ugroups[gps[s].X] : groups[gps[s].X];
-        const Group& gy = fam ? ugroups[gps[s].Y] : groups[gps[s].Y];
-        const std::vector<double>& QQ = fam ? uQ : Q;
-        const bool same = gps[s].X == gps[s].Y;
-        const int cbase = static_cast<int>(cnt.size());
-        long long total = 0;
-        for (int r = 0; r < gx.count; ++r) {
-          const int x = gx.first + r;
-          long long n = gy.count;
-          if (t > 0.0) {
-            // survivors: prefix of the Q-descending ket group
-            const double qx = QQ[x];
-            int lo = 0, hi = gy.count;
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              if (qx * QQ[gy.first + mid] >= t) lo = mid + 1;
-              else hi = mid;
+      cw.astrip_off = static_cast<long long>(all_strips.size());
+      const bool strip_ok = has_strip_variant(cls, fam);
+      const std::vector<double>& QQ = fam ? uQ : Q;
+      bra_tot.assign(fam ? um.size() : pm.size(), 0);
+      for (int sg = 0; sg < 4; ++sg) {
+        // the group pairs of this member segment (pair lists: segment 0 only)
+        size_t e = s;
+        while (e < gps.size() && gps[e].cls == cls && gps[e].fam == fam && gps[e].seg == sg) ++e;
+        cw.aseg[sg] = static_cast<long long>(all_items.size()) - cw.aoff;
+        cw.asseg[sg] = static_cast<long long>(all_strips.size()) - cw.astrip_off;
+        // survivor counts per (group pair, bra): prefix of the Q-descending ket group
+        std::vector<int> cfull(e - s);
+        for (size_t g = s; g < e; ++g) {
+          const Group& gx = fam ? ugroups[gps[g].X] : groups[gps[g].X];
+          const Group& gy = fam ? ugroups[gps[g].Y] : groups[gps[g].Y];
+          const bool same = gps[g].X == gps[g].Y;
+          cfull[g - s] = static_cast<int>(cnt.size());
+          for (int r = 0; r < gx.count; ++r) {
+            const int x = gx.first + r;
+            long long nn = gy.count;
+            if (t > 0.0) {
+              const double qx = QQ[x];
+              int lo = 0, hi = gy.count;
+              while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (qx * QQ[gy.first + mid] >= t) lo = mid + 1;
+                else hi = mid;
+              }
+              nn = lo;
             }
-            n = lo;
+            if (same) nn = std::min<long long>(nn, r + 1);
+            cnt.push_back(static_cast<int>(nn));
+            bra_tot[x] += nn;
           }
-          if (same) n = std::min<long long>(n, r + 1);
-          cnt.push_back(static_cast<int>(n));
-          total += n;
+          cnt.push_back(0);  // sentinel
         }
-        cnt.push_back(0);  // sentinel
-        // cut the flat sequence into warp tasks of 32 (unit) quartets
-        int r = 0;      // current bra rank within gx
-        long long off = 0;  // offset within bra r's survivors
-        for (long long base = 0; base < total; base += 32) {
-          while (r < gx.count && off >= cnt[cbase + r]) {
-            off -= cnt[cbase + r];
-            ++r;
-          }
-          const int nq = static_cast<int>(std::min<long long>(32, total - base));
-          all_items.push_back(WorkItem{gx.first + r, static_cast<int>(off) | (nq << 24), cbase + r, gy.first});
+        auto eligible = [&](int x) { return strip_ok && bra_tot[x] >= kStripMinQuartets; };
+        auto emit = [&](int x, int cpos_, int off, int nq, int ygroup_first, const Group& gx, const Group& gy,
+                        int cb, int r) {
+          all_items.push_back(WorkItem{x, off | (nq << 24), cpos_, ygroup_first});
           int q = nq;
           if (fam) {  // member quartets of these nq unit pairs
             q = 0;
-            int rr = r, oo = static_cast<int>(off);
+            int rr = r, oo = off;
             for (int l = 0; l < nq; ++l, ++oo) {
-              while (oo >= cnt[cbase + rr]) {
-                oo -= cnt[cbase + rr];
+              while (oo >= cnt[cb + rr]) {
+                oo -= cnt[cb + rr];
                 ++rr;
               }
               q += unit_pair_quartets(gx.first + rr, gy.first + oo, t);
@@ -910,19 +964,102 @@ struct eritile_gpu {
           item_p.push_back(static_cast<unsigned>(nq * gx.K * gy.K));
           cw.aquartets += q;
           cw.aprim += static_cast<long long>(nq) * gx.K * gy.K;
-          off += 32;
+        };
+        // 1) strips: eligible bras, single-bra items grouped by bra (runs over
+        //    the segment's ket groups), cut into strips of <= kStripMaxItems
+        if (strip_ok) {
+          struct Run {
+            int x;
+            int g, r;  // group pair (relative to s), bra rank in gx
+          };
+          std::vector<Run> runs;
+          for (size_t g = s; g < e; ++g) {
+            const Group& gx = fam ? ugroups[gps[g].X] : groups[gps[g].X];
+            for (int r = 0; r < gx.count; ++r)
+              if (eligible(gx.first + r) && cnt[cfull[g - s] + r] > 0)
+                runs.push_back(Run{gx.first + r, static_cast<int>(g - s), r});
+          }
+          std::stable_sort(runs.begin(), runs.end(), [](const Run& a, const Run& b) { return a.x < b.x; });
+          for (size_t k = 0; k < runs.size();) {
+            const int x = runs[k].x;
+            Strip st{};
+            st.bra = x;
+            st.i0 = static_cast<int>(static_cast<long long>(all_items.size()) - cw.aoff);
+            for (; k < runs.size() && runs[k].x == x; ++k) {
+              const GP& gp = gps[s + runs[k].g];
+              const Group& gx = fam ? ugroups[gp.X] : groups[gp.X];
+              const Group& gy = fam ? ugroups[gp.Y] : groups[gp.Y];
+              const int cb = cfull[runs[k].g];
+              const int nn = cnt[cb + runs[k].r];
+              for (int o = 0; o < nn; o += 32) {
+                if (static_cast<long long>(all_items.size()) - cw.aoff - st.i0 >= kStripMaxItems) {
+                  st.i1 = static_cast<int>(static_cast<long long>(all_items.size()) - cw.aoff);
+                  push_strip(st, fam);
+                  st.i0 = st.i1;
+                }
+                emit(x, cb + runs[k].r, o, std::min(32, nn - o), gy.first, gx, gy, cb, runs[k].r);
+              }
+            }
+            st.i1 = static_cast<int>(static_cast<long long>(all_items.size()) - cw.aoff);
+            if (st.i1 > st.i0) push_strip(st, fam);
+          }
+        }
+        cw.asitem[sg] = static_cast<long long>(all_items.size()) - cw.aoff;
+        // 2) the other bras: flat survivor sequence per group pair cut into
+        //    warp tasks of 32 (unit) quartets that may span bras; eligible
+        //    bras count 0 in this copy of the counts so the walk skips them
+        for (size_t g = s; g < e; ++g) {
+          const Group& gx = fam ? ugroups[gps[g].X] : groups[gps[g].X];
+          const Group& gy = fam ? ugroups[gps[g].Y] : groups[gps[g].Y];
+          int cb = cfull[g - s];
+          long long total = 0;
+          bool any_el = false;
+          for (int r = 0; r < gx.count; ++r) any_el = any_el || eligible(gx.first + r);
+          if (any_el) {  // counts without the strip bras
+            const int cr = static_cast<int>(cnt.size());
+            for (int r = 0; r < gx.count; ++r) cnt.push_back(eligible(gx.first + r) ? 0 : cnt[cb + r]);
+            cnt.push_back(0);
+            cb = cr;
+          }
+          for (int r = 0; r < gx.count; ++r) total += cnt[cb + r];
+          int r = 0;
+          long long off = 0;
+          for (long long base = 0; base < total; base += 32) {
+            while (r < gx.count && off >= cnt[cb + r]) {
+              off -= cnt[cb + r];
+              ++r;
+            }
+            emit(gx.first + r, cb + r, static_cast<int>(off), static_cast<int>(std::min<long long>(32, total - base)),
+                 gy.first, gx, gy, cb, r);
+            off += 32;
+          }
+        }
+        for (size_t g = s; g < e; ++g) {  // reset the per-bra totals of this segment
+          const Group& gx = fam ? ugroups[gps[g].X] : groups[gps[g].X];
+          for (int r = 0; r < gx.count; ++r) bra_tot[gx.first + r] = 0;
+        }
+        s = e;
+        if (!fam) {  // pair lists have one segment
+          for (int k = sg + 1; k < 4; ++k) {
+            cw.aseg[k] = static_cast<long long>(all_items.size()) - cw.aoff;
+            cw.asseg[k] = static_cast<long long>(all_strips.size()) - cw.astrip_off;
+            cw.asitem[k] = cw.aseg[k];
+          }
+          break;
         }
       }
       cw.an = static_cast<long long>(all_items.size()) - cw.aoff;
-      while (cur_seg < 4) cw.aseg[++cur_seg] = cw.an;
+      cw.aseg[4] = cw.an;
+      cw.asseg[4] = static_cast<long long>(all_strips.size()) - cw.astrip_off;
       if (std::getenv("ERITILE_DEBUG_ITEMS") && cw.an > 0) {  // diagnostics: items spanning > 1 bra
         long long multi = 0;
         for (long long w = cw.aoff; w < cw.aoff + cw.an; ++w) {
           const WorkItem& it = all_items[w];
           if ((it.r0nq & 0xffffff) + (it.r0nq >> 24) > cnt[it.cntp]) ++multi;
         }
-        std::fprintf(stderr, "class %d fam %d items %lld multi-bra %.3f\n", cls, fam ? 1 : 0, cw.an,
-                     static_cast<double>(multi) / cw.an);
+        std::fprintf(stderr, "class %d fam %d items %lld multi-bra %.3f strips %lld strip items %lld\n", cls,
+                     fam ? 1 : 0, cw.an, static_cast<double>(multi) / cw.an, cw.asseg[4],
+                     cw.asitem[0] + cw.asitem[1] - cw.aseg[1] + cw.asitem[2] - cw.aseg[2] + cw.asitem[3] - cw.aseg[3]);
       }
       if (cw.an > 0) {
         const ClassEntry& ce = kClassTable[cls];
@@ -934,15 +1071,65 @@ struct eritile_gpu {
         cw.cost_prim = 42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract);
         cw.cost_q = 2.0 * ce.hrr_terms + 12.0 * nv;
         work.push_back(cw);
+      } else {
+        all_strips.resize(cw.astrip_off);
       }
     }
     if (!host_only) {
       d_cnt.upload(cnt, stream);
       d_all_items.upload(all_items, stream);
+      d_all_strips.upload(all_strips, stream);
     }
     have_lists = true;
     dealt = false;
     deal();
+  }
+
+  // Strip geometry: row blocks = the distinct shells of the bra members.
+  long long kStripMinQuartets = 1024;  // bras with fewer survivors stay packed
+  long long kStripMaxItems = 256;      // items per strip (granularity / load balance)
+  void push_strip(Strip st, bool fam) {
+    int mem[2], nm = 1;
+    if (fam) {
+      mem[0] = um[st.bra].m0;
+      mem[1] = um[st.bra].m1;
+      nm = um[st.bra].nm;
+    } else {
+      mem[0] = st.bra;
+    }
+    int nb = 0, row = 0;
+    int shl[4];
+    auto row_of = [&](int sh) {
+      for (int k = 0; k < nb; ++k)
+        if (shl[k] == sh) {
+          int r = 0;
+          for (int q = 0; q < k; ++q) r += st.rb_n[q];
+          return r;
+        }
+      shl[nb] = sh;
+      st.rb_bf[nb] = bf_off[sh];
+      st.rb_n[nb] = shells[sh].nfunc();
+      const int r = row;
+      row += st.rb_n[nb];
+      ++nb;
+      return r;
+    };
+    for (int m = 0; m < nm; ++m) {
+      st.rowA[m] = row_of(pm[mem[m]].sha);
+      st.rowB[m] = row_of(pm[mem[m]].shb);
+    }
+    for (int k = nb; k < 4; ++k) {
+      st.rb_bf[k] = 0;
+      st.rb_n[k] = 0;
+    }
+    st.nrows = row;
+    all_strips.push_back(st);
+  }
+  bool has_strip_variant(int c, bool fam) const {
+    const ClassEntry& ce = kClassTable[c];
+    for (int v = 0; v < ce.nvar; ++v)
+      if (std::strncmp(ce.var_name[v], fam ? "fstrip" : "strip", fam ? 6 : 5) == 0) return true;
+    return false;
   }
 
   // Quartet-block sharding (quartets are independent,
@@ -964,17 +1151,25 @@ struct eritile_gpu {
         cw.off = cw.aoff;
         cw.n = cw.an;
         for (int k = 0; k < 5; ++k) cw.seg[k] = cw.aseg[k];
+        for (int k = 0; k < 5; ++k) cw.sseg[k] = cw.asseg[k];
+        for (int k = 0; k < 4; ++k) cw.sitem[k] = cw.asitem[k];
+        cw.strip_off = cw.astrip_off;
         cw.quartets = cw.aquartets;
         cw.prim_quartets = cw.aprim;
         cw.flops = cw.full_flops();
       }
       items.clear();
+      strips.clear();
       update_totals();
       dealt = true;
       return;
     }
+    // chunks: every strip whole (its K rows are flushed per strip), then the
+    // packed items of each segment in runs of kDealChunk
     struct Chunk {
       long long b, e;  // all_items range
+      long long strip; // all_strips index, -1 for packed items
+      int sg;
       double w;
       int owner;
     };
@@ -983,16 +1178,22 @@ struct eritile_gpu {
     for (size_t w = 0; w < work.size(); ++w) {
       const ClassWork& cw = work[w];
       wch[w].first = ch.size();
+      auto weight = [&](long long b, long long e) {
+        double wt = 0.0;
+        for (long long i = b; i < e; ++i) wt += cw.cost_prim * item_p[i] + cw.cost_q * item_q[i];
+        return wt;
+      };
       if (active(cw)) {
-        const int nseg = cw.fam ? 4 : 1;
-        for (int sg = 0; sg < nseg; ++sg) {
-          const long long s0 = cw.aoff + (cw.fam ? cw.aseg[sg] : 0);
-          const long long s1 = cw.aoff + (cw.fam ? cw.aseg[sg + 1] : cw.an);
+        for (int sg = 0; sg < 4; ++sg) {
+          for (long long k = cw.asseg[sg]; k < cw.asseg[sg + 1]; ++k) {
+            const Strip& st = all_strips[cw.astrip_off + k];
+            const long long b = cw.aoff + st.i0, e = cw.aoff + st.i1;
+            ch.push_back(Chunk{b, e, cw.astrip_off + k, sg, weight(b, e), 0});
+          }
+          const long long s0 = cw.aoff + cw.asitem[sg], s1 = cw.aoff + cw.aseg[sg + 1];
           for (long long b = s0; b < s1; b += kDealChunk) {
             const long long e = std::min(s1, b + kDealChunk);
-            double wt = 0.0;
-            for (long long i = b; i < e; ++i) wt += cw.cost_prim * item_p[i] + cw.cost_q * item_q[i];
-            ch.push_back(Chunk{b, e, wt, 0});
+            ch.push_back(Chunk{b, e, -1, sg, weight(b, e), 0});
           }
         }
       }
@@ -1010,27 +1211,49 @@ struct eritile_gpu {
       load[r] += ch[k].w;
     }
     items.clear();
+    strips.clear();
     for (size_t w = 0; w < work.size(); ++w) {
       ClassWork& cw = work[w];
       cw.off = static_cast<long long>(items.size());
+      cw.strip_off = static_cast<long long>(strips.size());
       cw.quartets = cw.prim_quartets = 0;
-      for (int k = 0; k < 5; ++k) cw.seg[k] = 0;
-      int sg = 0;
-      for (size_t k = wch[w].first; k < wch[w].second; ++k) {
-        const Chunk& c = ch[k];
-        while (cw.fam && sg < 4 && c.b - cw.aoff >= cw.aseg[sg + 1]) cw.seg[++sg] = static_cast<long long>(items.size()) - cw.off;
-        if (c.owner != rank) continue;
-        for (long long i = c.b; i < c.e; ++i) {
-          items.push_back(all_items[i]);
-          cw.quartets += item_q[i];
-          cw.prim_quartets += item_p[i];
+      for (int k = 0; k < 5; ++k) cw.seg[k] = cw.sseg[k] = 0;
+      for (int k = 0; k < 4; ++k) cw.sitem[k] = 0;
+      size_t k = wch[w].first;
+      for (int sg = 0; sg < 4; ++sg) {
+        cw.seg[sg] = static_cast<long long>(items.size()) - cw.off;
+        cw.sseg[sg] = static_cast<long long>(strips.size()) - cw.strip_off;
+        bool rest = false;
+        for (; k < wch[w].second && ch[k].sg == sg; ++k) {
+          const Chunk& c = ch[k];
+          if (c.strip < 0 && !rest) {
+            cw.sitem[sg] = static_cast<long long>(items.size()) - cw.off;
+            rest = true;
+          }
+          if (c.owner != rank) continue;
+          if (c.strip >= 0) {
+            Strip st = all_strips[c.strip];
+            st.i0 = static_cast<int>(static_cast<long long>(items.size()) - cw.off);
+            st.i1 = st.i0 + static_cast<int>(c.e - c.b);
+            strips.push_back(st);
+          }
+          for (long long i = c.b; i < c.e; ++i) {
+            items.push_back(all_items[i]);
+            cw.quartets += item_q[i];
+            cw.prim_quartets += item_p[i];
+          }
         }
+        if (!rest) cw.sitem[sg] = static_cast<long long>(items.size()) - cw.off;
       }
       cw.n = static_cast<long long>(items.size()) - cw.off;
-      while (sg < 4) cw.seg[++sg] = cw.n;
+      cw.seg[4] = cw.n;
+      cw.sseg[4] = static_cast<long long>(strips.size()) - cw.strip_off;
       cw.flops = cw.cost_prim * static_cast<double>(cw.prim_quartets) + cw.cost_q * static_cast<double>(cw.quartets);
     }
-    if (!host_only) d_items.upload(items, stream);
+    if (!host_only) {
+      d_items.upload(items, stream);
+      d_strips.upload(strips, stream);
+    }
     update_totals();
     dealt = true;
   }
@@ -1715,6 +1938,14 @@ int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var) {
   if (ctx->var_choice.empty()) ctx->var_choice.assign(kNumClasses, -1);
   ctx->var_choice[cls_index] = var;
   ctx->dealt = false;  // the active lists (pair / unit) may change: re-deal
+  return ERITILE_OK;
+}
+
+int eritile_gpu_set_strips(eritile_gpu* ctx, long long min_quartets, int max_items) {
+  if (!ctx || min_quartets < 1 || max_items < 1) return ERITILE_ERR_ARG;
+  ctx->kStripMinQuartets = min_quartets;
+  ctx->kStripMaxItems = max_items;
+  ctx->have_lists = false;
   return ERITILE_OK;
 }
 

@@ -57,10 +57,11 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
   for (long long s = s0 + blockIdx.x; s < s1; s += gridDim.x) {
     const Strip st = a.strips[s];
     const int nrows = st.nrows;
-    if (threadIdx.x < 4) {
+    if (threadIdx.x < 4) {  // (indexed through global memory: no local copy of st)
+      const Strip* gs = a.strips + s;
       int r = 0;
-      for (int k = 0; k < static_cast<int>(threadIdx.x); ++k) r += st.rb_n[k];
-      for (int t = 0; t < st.rb_n[threadIdx.x]; ++t) s_rowg[r + t] = st.rb_bf[threadIdx.x] + t;
+      for (int k = 0; k < static_cast<int>(threadIdx.x); ++k) r += gs->rb_n[k];
+      for (int t = 0; t < gs->rb_n[threadIdx.x]; ++t) s_rowg[r + t] = gs->rb_bf[threadIdx.x] + t;
     }
     // bra records (and unit weights): one copy per CTA for the whole strip
     int kb, boff;

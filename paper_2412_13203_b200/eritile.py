@@ -93,6 +93,7 @@ def _lib():
         "eritile_gpu_tune_times": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
         "eritile_gpu_set_families": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_set_concurrent": (C.c_int, [C.c_void_p, C.c_int]),
+        "eritile_gpu_set_strips": (C.c_int, [C.c_void_p, C.c_longlong, C.c_int]),
         "eritile_gpu_variant_range": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "eritile_gpu_get_variant": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_class_nvariants": (C.c_int, [C.c_int]),
@@ -330,6 +331,12 @@ class Engine:
         """Shared-primitive units for generally contracted sibling shells
         (csrc/jk_family.cuh); takes effect at the next set_screening."""
         self._check(self._lib.eritile_gpu_set_families(self._h, int(on)))
+        return self
+
+    def set_strips(self, min_quartets: int = 1024, max_items: int = 256) -> "Engine":
+        """Strip layout of the work lists (csrc/jk_strip.cuh); takes effect at
+        the next set_screening."""
+        self._check(self._lib.eritile_gpu_set_strips(self._h, int(min_quartets), int(max_items)))
         return self
 
     def set_concurrent(self, on: bool = True) -> "Engine":
