@@ -172,7 +172,7 @@ int eritile_gpu_set_variants(eritile_gpu* ctx, const int* var, int n);
 int eritile_gpu_set_families(eritile_gpu* ctx, int on);
 /* Strip lists (bra-stationary CTAs, K rows in shared memory): bras with at
  * least min_quartets survivors in a class get single-bra items grouped into
- * strips of at most max_items warp tasks (defaults 1024, 256); the rest stay
+ * strips of at most max_items warp tasks (defaults 1024, 1024); the rest stay
  * packed. Takes effect at the next set_screening; lists and results are
  * unchanged, only the work layout. */
 int eritile_gpu_set_strips(eritile_gpu* ctx, long long min_quartets, int max_items);

@@ -286,6 +286,7 @@ def variants(info) -> List[Tuple[str, str]]:
         # the packed multi-bra remainder runs on a lane kernel
         if info["ops"] <= MINB_SMALL_OPS:
             out.append(("strip_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512>"))
+            out.append(("strip_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
         if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:

@@ -944,7 +944,9 @@ struct eritile_gpu {
           }
           cnt.push_back(0);  // sentinel
         }
-        auto eligible = [&](int x) { return strip_ok && bra_tot[x] >= kStripMinQuartets; };
+        auto eligible = [&](int x) {
+          return strip_ok && bra_tot[x] >= kStripMinQuartets && (fam ? um[x].K : pm[x].K) <= kStripBraMax;
+        };
         auto emit = [&](int x, int cpos_, int off, int nq, int ygroup_first, const Group& gx, const Group& gy,
                         int cb, int r) {
           all_items.push_back(WorkItem{x, off | (nq << 24), cpos_, ygroup_first});
@@ -1087,7 +1089,7 @@ struct eritile_gpu {
 
   // Strip geometry: row blocks = the distinct shells of the bra members.
   long long kStripMinQuartets = 1024;  // bras with fewer survivors stay packed
-  long long kStripMaxItems = 256;      // items per strip (granularity / load balance)
+  long long kStripMaxItems = 1024;     // items per strip (granularity / load balance)
   void push_strip(Strip st, bool fam) {
     int mem[2], nm = 1;
     if (fam) {

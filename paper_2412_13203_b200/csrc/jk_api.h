@@ -55,6 +55,8 @@ struct alignas(16) UnitMeta {
 // shared memory. Row blocks: the distinct shells of the bra members, in
 // shared-memory row order (rb_n = 0 unused); rowA/rowB: shared-memory row of
 // member m's first A / B component.
+constexpr int kStripBraMax = 128;  // strip bras: primitive pairs staged in shared memory
+
 struct alignas(16) Strip {
   int bra, i0, i1, nrows;
   int rowA[2], rowB[2];

@@ -33,7 +33,7 @@ template <class C, int MB>
 struct StripSmem {
   static constexpr int kRowsMax = MB * (C::NA + C::NB);
   static size_t bytes(int ncols, bool dsm) {
-    return BoysStage<C>::bytes + (sizeof(PrimRec) + sizeof(double2)) * kSmemBraMax +
+    return BoysStage<C>::bytes + (sizeof(PrimRec) + sizeof(double2)) * kStripBraMax +
            sizeof(double) * static_cast<size_t>(kRowsMax) * ncols * (dsm ? 2 : 1);
   }
 };
@@ -44,11 +44,13 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
   load_boys_for<C>(smem, a.boys_tab);
   constexpr int kBoysD = BoysStage<C>::nsl * kBoysRows * kBoysCols;
   PrimRec* sbra = reinterpret_cast<PrimRec*>(smem + kBoysD);
-  double2* sbw = reinterpret_cast<double2*>(sbra + kSmemBraMax);
-  double* sK = reinterpret_cast<double*>(sbw + kSmemBraMax);
+  double2* sbw = reinterpret_cast<double2*>(sbra + kStripBraMax);
+  double* sK = reinterpret_cast<double*>(sbw + kStripBraMax);
   const int ncol = a.ncols;
   double* sD = sK + StripSmem<C, MB>::kRowsMax * ncol;
   __shared__ int s_rowg[StripSmem<C, MB>::kRowsMax];  // global basis function of each smem row
+  __shared__ int s_bm[MB][4];                         // bra members: bfa, bfb, sha, shb
+  __shared__ int s_next;                              // next item of the strip (dynamic hand-out)
   (void)sD;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
@@ -64,6 +66,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       for (int t = 0; t < gs->rb_n[threadIdx.x]; ++t) s_rowg[r + t] = gs->rb_bf[threadIdx.x] + t;
     }
     // bra records (and unit weights): one copy per CTA for the whole strip
+    // (strip bras have K <= kStripBraMax; the host keeps larger ones packed)
     int kb, boff;
     if constexpr (FAM) {
       kb = a.um[st.bra].K;
@@ -72,14 +75,24 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       kb = a.pm[st.bra].K;
       boff = a.pm[st.bra].prim_off;
     }
-    const bool bsm = kb <= kSmemBraMax;
-    if (bsm) {
+    {
       const double2* src = reinterpret_cast<const double2*>(a.prims + boff);
       double2* dst = reinterpret_cast<double2*>(sbra);
       for (int t = threadIdx.x; t < kb * 5; t += NT) dst[t] = __ldg(src + t);
       if constexpr (FAM)
         for (int t = threadIdx.x; t < kb; t += NT) sbw[t] = __ldg(a.uw + boff + t);
     }
+    if (threadIdx.x < MB) {
+      int px = st.bra;
+      if constexpr (FAM) px = threadIdx.x == 0 ? a.um[st.bra].m0 : a.um[st.bra].m1;
+      PairMeta bm;
+      ld_meta_late(a.pm + px, bm);
+      s_bm[threadIdx.x][0] = bm.bfa;
+      s_bm[threadIdx.x][1] = bm.bfb;
+      s_bm[threadIdx.x][2] = bm.sha;
+      s_bm[threadIdx.x][3] = bm.shb;
+    }
+    if (threadIdx.x == 0) s_next = st.i0;
     for (int e = threadIdx.x; e < nrows * ncol; e += NT) sK[e] = 0.0;
     __syncthreads();
     if constexpr (DSM) {
@@ -89,8 +102,8 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       }
       __syncthreads();
     }
-    const PrimRec* brap = bsm ? sbra : a.prims + boff;
-    const double2* bwp = bsm ? sbw : a.uw + boff;
+    const PrimRec* brap = sbra;
+    const double2* bwp = sbw;
     (void)bwp;
     // J_ab partial sums, lane-private over all items of the strip
     double jab[MB][C::NA * C::NB];
@@ -106,7 +119,12 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
     } else {
       bpx[0] = st.bra;
     }
-    for (long long w = st.i0 + warp; w < st.i1; w += NW) {
+    (void)warp;
+    for (;;) {
+      int w = 0;
+      if (lane == 0) w = atomicAdd(&s_next, 1);  // dynamic: items differ in primitive count
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (w >= st.i1) break;
       const WorkItem it = a.items[w];
       const int nq = it.r0nq >> 24;
       const bool active = lane < nq;
@@ -144,7 +162,10 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
       for (int m = 0; m < MB; ++m) {
         PairMeta bm;
-        ld_meta_late(a.pm + bpx[m], bm);
+        bm.bfa = s_bm[m][0];
+        bm.bfb = s_bm[m][1];
+        bm.sha = s_bm[m][2];
+        bm.shb = s_bm[m][3];
         const int rA = st.rowA[m], rB = st.rowB[m];
 #pragma unroll
         for (int k = 0; k < MK; ++k) {
@@ -251,14 +272,13 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
     // J_ab: one butterfly per strip and warp, one RED per element and warp
 #pragma unroll
     for (int m = 0; m < MB; ++m) {
-      PairMeta bm;
-      ld_meta_late(a.pm + bpx[m], bm);
+      const size_t bfa = s_bm[m][0], bfb = s_bm[m][1];
 #pragma unroll
       for (int e = 0; e < C::NA * C::NB; ++e) {
         double t = jab[m][e];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0 && t != 0.0) red_add(a.J + (bm.bfa + e / C::NB) * n + bm.bfb + e % C::NB, t);
+        if (lane == 0 && t != 0.0) red_add(a.J + (bfa + e / C::NB) * n + bfb + e % C::NB, t);
       }
     }
     __syncthreads();

@@ -333,7 +333,7 @@ class Engine:
         self._check(self._lib.eritile_gpu_set_families(self._h, int(on)))
         return self
 
-    def set_strips(self, min_quartets: int = 1024, max_items: int = 256) -> "Engine":
+    def set_strips(self, min_quartets: int = 1024, max_items: int = 1024) -> "Engine":
         """Strip layout of the work lists (csrc/jk_strip.cuh); takes effect at
         the next set_screening."""
         self._check(self._lib.eritile_gpu_set_strips(self._h, int(min_quartets), int(max_items)))
