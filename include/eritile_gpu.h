@@ -34,6 +34,15 @@ enum {
   ERITILE_ERR_DOMAIN = -5   /* std::domain_error (boys.hpp:48-50) */
 };
 
+/* build_g reduction modes (SPEC.md executor, Accumulator): concurrent FP64
+ * atomics (default), or deterministic - contributions are rounded to
+ * multiples of 2^-44 and summed as 64-bit integers, exact and independent of
+ * scheduling, so results are bitwise reproducible for a given variant table
+ * (|J|, |K| accumulators < 2^19). In deterministic mode the partial
+ * accumulators of build_jk_partial_device hold int64 values: sum them across
+ * ranks as int64. Strip variants run their items on the lane kernels. */
+enum { ERITILE_MODE_CONCURRENT = 0, ERITILE_MODE_DETERMINISTIC = 1 };
+
 typedef struct eritile_gpu_stats {
   int nbf, nshells, npairs, nclasses;
   long long quartets;        /* surviving canonical quartets on this rank */
@@ -85,6 +94,8 @@ int eritile_gpu_build_pairs(eritile_gpu* ctx, double kappa_screen);
 int eritile_gpu_npairs(const eritile_gpu* ctx);
 /* Reference pair-store order: shells (i<=j) of pair x, x < npairs. */
 int eritile_gpu_pair_shells(const eritile_gpu* ctx, int* i, int* j);
+/* Kept primitive pairs of each pair (ShellPair::prims.size(), block.hpp:26-31). */
+int eritile_gpu_pair_nprims(const eritile_gpu* ctx, int* nprim);
 
 /* Schwarz diagonal on the GPU; Q per pair in reference pair-store order
  * (Q may be NULL). Not in the reference. */
@@ -176,6 +187,9 @@ int eritile_gpu_set_families(eritile_gpu* ctx, int on);
  * packed. Takes effect at the next set_screening; lists and results are
  * unchanged, only the work layout. */
 int eritile_gpu_set_strips(eritile_gpu* ctx, long long min_quartets, int max_items);
+/* Reduction mode, ERITILE_MODE_* (takes effect at the next build). */
+int eritile_gpu_set_mode(eritile_gpu* ctx, int mode);
+int eritile_gpu_get_mode(const eritile_gpu* ctx);
 /* Class launches of a build on 4 streams (default) or on one stream. */
 int eritile_gpu_set_concurrent(eritile_gpu* ctx, int on);
 /* Active variant index range [lo, hi) of a class in this context. */

@@ -133,16 +133,25 @@ __global__ void k_prescale(const double* __restrict__ D, const double* __restric
 }
 
 // true J = s_mu s_nu (Jacc + Jacc^T)/2, true K likewise (Appendix C).
+// det: the accumulators hold int64 fixed point (kDetScale, red_add).
 __global__ void k_finalize(const double* __restrict__ Jacc, const double* __restrict__ Kacc,
                            const double* __restrict__ s, double* __restrict__ J, double* __restrict__ K,
-                           int N) {
+                           int N, int det) {
   const size_t NN = static_cast<size_t>(N) * N;
+  const long long* Ji = reinterpret_cast<const long long*>(Jacc);
+  const long long* Ki = reinterpret_cast<const long long*>(Kacc);
+  const double inv = 1.0 / kDetScale;
   for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < NN;
        e += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t r = e / N, c = e % N, t = c * N + r;
     const double f = 0.5 * (s[r] * s[c]);
-    J[e] = f * (Jacc[e] + Jacc[t]);
-    K[e] = f * (Kacc[e] + Kacc[t]);
+    if (det) {
+      J[e] = f * (static_cast<double>(Ji[e]) * inv + static_cast<double>(Ji[t]) * inv);
+      K[e] = f * (static_cast<double>(Ki[e]) * inv + static_cast<double>(Ki[t]) * inv);
+    } else {
+      J[e] = f * (Jacc[e] + Jacc[t]);
+      K[e] = f * (Kacc[e] + Kacc[t]);
+    }
   }
 }
 
@@ -326,6 +335,7 @@ struct eritile_gpu {
   std::vector<double> tune_ms;  // per class launch x kMaxVariants: median ms (tune)
 
   bool profiling = false;
+  bool det = false;  // deterministic reduction mode (fixed-point integer atomics)
   bool host_only = false;  // device < 0: block constructor / lists only
   std::vector<cudaEvent_t> prof_ev;
 
@@ -415,6 +425,7 @@ struct eritile_gpu {
     LaunchArgs a{};
     a.mode = 0;
     const bool use_all = full || nranks == 1;
+    a.det = det ? 1 : 0;
     a.items = use_all ? d_all_items.p + cw.aoff : d_items.p + cw.off;
     a.nitems = full ? cw.an : cw.n;
     a.cnt = d_cnt.p;
@@ -1341,7 +1352,7 @@ struct eritile_gpu {
   void finalize(const double* dJK, double* dJ, double* dK, cudaStream_t st) {
     const size_t NN = static_cast<size_t>(nbf) * nbf;
     const int grid = static_cast<int>(std::min<size_t>((NN + 255) / 256, 148 * 32));
-    k_finalize<<<std::max(grid, 1), 256, 0, st>>>(dJK, dJK + NN, d_scale.p, dJ, dK, nbf);
+    k_finalize<<<std::max(grid, 1), 256, 0, st>>>(dJK, dJK + NN, d_scale.p, dJ, dK, nbf, det ? 1 : 0);
     CK(cudaGetLastError());
   }
 
@@ -1948,6 +1959,22 @@ int eritile_gpu_set_strips(eritile_gpu* ctx, long long min_quartets, int max_ite
   ctx->kStripMinQuartets = min_quartets;
   ctx->kStripMaxItems = max_items;
   ctx->have_lists = false;
+  return ERITILE_OK;
+}
+
+int eritile_gpu_set_mode(eritile_gpu* ctx, int mode) {
+  if (!ctx || (mode != ERITILE_MODE_CONCURRENT && mode != ERITILE_MODE_DETERMINISTIC))
+    return fail(ctx, ERITILE_ERR_ARG, "set_mode: mode must be concurrent (0) or deterministic (1)");
+  ctx->det = mode == ERITILE_MODE_DETERMINISTIC;
+  return ERITILE_OK;
+}
+int eritile_gpu_get_mode(const eritile_gpu* ctx) {
+  return ctx ? (ctx->det ? ERITILE_MODE_DETERMINISTIC : ERITILE_MODE_CONCURRENT) : ERITILE_ERR_ARG;
+}
+
+int eritile_gpu_pair_nprims(const eritile_gpu* ctx, int* nprim) {
+  if (!ctx || !nprim) return ERITILE_ERR_ARG;
+  for (size_t r = 0; r < ctx->pm.size(); ++r) nprim[r] = ctx->pm[ctx->prod_of_ref[r]].K;
   return ERITILE_OK;
 }
 

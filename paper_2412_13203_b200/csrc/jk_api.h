@@ -55,7 +55,13 @@ struct alignas(16) UnitMeta {
 // shared memory. Row blocks: the distinct shells of the bra members, in
 // shared-memory row order (rb_n = 0 unused); rowA/rowB: shared-memory row of
 // member m's first A / B component.
-constexpr int kStripBraMax = 128;  // strip bras: primitive pairs staged in shared memory
+constexpr int kStripBraMax = 128;
+// Deterministic reduction mode (SPEC.md executor "deterministic" accumulator):
+// every J/K contribution is rounded to a multiple of 2^-44 and added as a
+// 64-bit integer, so the sums are exact and independent of atomic order
+// (bitwise reproducible). Range |Jacc|, |Kacc| < 2^19 (two's complement wrap
+// of partial sums is harmless); rounding error <= 2^-45 per contribution.
+constexpr double kDetScale = 17592186044416.0;  // 2^44  // strip bras: primitive pairs staged in shared memory
 
 struct alignas(16) Strip {
   int bra, i0, i1, nrows;
@@ -100,6 +106,7 @@ struct LaunchArgs {
   const Strip* strips;
   long long sseg[5];
   long long sitem[4];
+  int det;          // deterministic mode: J/K accumulate as int64 fixed point (kDetScale)
   const int* cols;  // compact K/D column list of the class: L_C functions (++ L_D functions if L_D != L_C)
   const int* cpos;  // per shell: first compact column within its own L list
   int ncols, ncolC;

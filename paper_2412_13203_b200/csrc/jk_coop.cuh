@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(C::NT) coop_kernel(CoopTables tb, LaunchArgs a
           dst = a.K + (bm.bfb + ib) * n + km.bfa + ic;
           s *= wk;
         }
-        atomicAdd(dst, s);
+        red_add(dst, s, a.det);
       }
       __syncthreads();
     }
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(32 * kCoopWarps) coopw_kernel(CoopTables tb, L
           dst = a.K + (bm.bfb + ib) * n + km.bfa + ic;
           s *= wk;
         }
-        red_add(dst, s);
+        red_add(dst, s, a.det);
       }
       __syncwarp();
     }

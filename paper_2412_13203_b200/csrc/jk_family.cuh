@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 #pragma unroll
                 for (int ib = 0; ib < C::NB; ++ib)
                   s = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), s);
-              red_add(a.J + (km.bfa + ic) * n + km.bfb + id, s * wj);
+              red_add(a.J + (km.bfa + ic) * n + km.bfb + id, s * wj, a.det);
             }
 #pragma unroll
           for (int ia = 0; ia < C::NA; ++ia)
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 #pragma unroll
                 for (int id = 0; id < C::ND; ++id)
                   s = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dbd + ib * n + id), s);
-              red_add(a.K + (bm.bfa + ia) * n + km.bfa + ic, s * wk);
+              red_add(a.K + (bm.bfa + ia) * n + km.bfa + ic, s * wk, a.det);
             }
 #pragma unroll
           for (int ib = 0; ib < C::NB; ++ib)
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 #pragma unroll
                 for (int ic = 0; ic < C::NC; ++ic)
                   s = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dac + ia * n + ic), s);
-              red_add(a.K + (bm.bfb + ib) * n + km.bfb + id, s * wk);
+              red_add(a.K + (bm.bfb + ib) * n + km.bfb + id, s * wk, a.det);
             }
 #pragma unroll
           for (int ia = 0; ia < C::NA; ++ia)
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 #pragma unroll
                 for (int ic = 0; ic < C::NC; ++ic)
                   s = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dbc + ib * n + ic), s);
-              red_add(a.K + (bm.bfa + ia) * n + km.bfb + id, s * wk);
+              red_add(a.K + (bm.bfa + ia) * n + km.bfb + id, s * wk, a.det);
             }
 #pragma unroll
           for (int ib = 0; ib < C::NB; ++ib)
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 #pragma unroll
                 for (int id = 0; id < C::ND; ++id)
                   s = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dad + ia * n + id), s);
-              red_add(a.K + (bm.bfb + ib) * n + km.bfa + ic, s * wk);
+              red_add(a.K + (bm.bfb + ib) * n + km.bfa + ic, s * wk, a.det);
             }
         }
       }
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
 #pragma unroll
         for (int ib = 0; ib < C::NB; ++ib) {
           const double s = seg_sum(jab[ia * C::NB + ib], xkey, lane);
-          if (tail && s != 0.0) red_add(a.J + (bm.bfa + ia) * n + bm.bfb + ib, s);
+          if (tail && s != 0.0) red_add(a.J + (bm.bfa + ia) * n + bm.bfb + ib, s, a.det);
         }
     }
   }

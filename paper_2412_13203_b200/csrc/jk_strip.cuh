@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
                 for (int ib = 0; ib < C::NB; ++ib)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), t);
-              red_add(a.J + (km.bfa + ic) * n + km.bfb + id, t * wj);
+              red_add(a.J + (km.bfa + ic) * n + km.bfb + id, t * wj, 0);
             }
           // K_ac += sum_bd v D_bd ; K_ad += sum_bc v D_bc   (rows a of the bra)
 #pragma unroll
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         double t = jab[m][e];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0 && t != 0.0) red_add(a.J + (bfa + e / C::NB) * n + bfb + e % C::NB, t);
+        if (lane == 0 && t != 0.0) red_add(a.J + (bfa + e / C::NB) * n + bfb + e % C::NB, t, 0);
       }
     }
     __syncthreads();
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       const double v = sK[e];
       if (v != 0.0) {
         const int r = e / ncol;
-        red_add(a.K + static_cast<size_t>(s_rowg[r]) * n + __ldg(a.cols + (e - r * ncol)), v);
+        red_add(a.K + static_cast<size_t>(s_rowg[r]) * n + __ldg(a.cols + (e - r * ncol)), v, 0);
       }
     }
     __syncthreads();
@@ -321,10 +321,13 @@ bool launch_strip_seg(const LaunchArgs& a, long long s0, long long s1) {
 
 // Pair-list strip variant: strips through the strip kernel, the remaining
 // (multi-bra packed) items through the lane kernel <MINB, STYLE, NTL>.
+// Deterministic mode runs every item on the lane kernels (the shared-memory
+// K rows would sum in scheduling order).
 template <class C, int NT, int MINB, int STYLE, int NTL>
 void launch_strip(const LaunchArgs& a) {
   if (a.mode != 0) return launch_class<C, 2, kLoopPrefetch>(a);
   if (a.nitems <= 0) return;
+  if (a.det) return launch_class<C, MINB, STYLE, NTL>(a);
   LaunchArgs r = a;
   if (launch_strip_seg<C, false, 1, 1, NT>(a, a.sseg[0], a.sseg[1])) {
     r.items = a.items + a.sitem[0];
@@ -338,6 +341,13 @@ void launch_strip(const LaunchArgs& a) {
 template <class C, int NT, int MINB, int STYLE, int NTL, int NT11>
 void launch_fstrip(const LaunchArgs& a) {
   if (a.mode != 0) return launch_class<C, 2, kLoopPrefetch>(a);
+  if (a.det) {
+    launch_fam_seg<C, 1, 1, MINB, STYLE, NT11>(a, a.seg[0], a.seg[1]);
+    launch_fam_seg<C, 1, 2, MINB, STYLE, NTL>(a, a.seg[1], a.seg[2]);
+    launch_fam_seg<C, 2, 1, MINB, STYLE, NTL>(a, a.seg[2], a.seg[3]);
+    launch_fam_seg<C, 2, 2, MINB, STYLE, NTL>(a, a.seg[3], a.seg[4]);
+    return;
+  }
   long long rest0[4];
   for (int sg = 0; sg < 4; ++sg) rest0[sg] = a.seg[sg];
   if (launch_strip_seg<C, true, 1, 1, NT>(a, a.sseg[0], a.sseg[1])) rest0[0] = a.sitem[0];

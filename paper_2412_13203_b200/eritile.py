@@ -94,6 +94,9 @@ def _lib():
         "eritile_gpu_set_families": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_set_concurrent": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_set_strips": (C.c_int, [C.c_void_p, C.c_longlong, C.c_int]),
+        "eritile_gpu_set_mode": (C.c_int, [C.c_void_p, C.c_int]),
+        "eritile_gpu_get_mode": (C.c_int, [C.c_void_p]),
+        "eritile_gpu_pair_nprims": (C.c_int, [C.c_void_p, _ip]),
         "eritile_gpu_variant_range": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "eritile_gpu_get_variant": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_class_nvariants": (C.c_int, [C.c_int]),
@@ -338,6 +341,23 @@ class Engine:
         the next set_screening."""
         self._check(self._lib.eritile_gpu_set_strips(self._h, int(min_quartets), int(max_items)))
         return self
+
+    def set_mode(self, mode: str = "concurrent") -> "Engine":
+        """build_g reduction mode (SPEC.md executor): "concurrent" (FP64
+        atomics) or "deterministic" (fixed-point integer sums, bitwise
+        reproducible)."""
+        m = {"concurrent": 0, "deterministic": 1}[mode]
+        self._check(self._lib.eritile_gpu_set_mode(self._h, m))
+        return self
+
+    @property
+    def mode(self) -> str:
+        return ["concurrent", "deterministic"][self._lib.eritile_gpu_get_mode(self._h)]
+
+    def pair_nprims(self) -> np.ndarray:
+        n = np.zeros(self.npairs, np.int32)
+        self._check(self._lib.eritile_gpu_pair_nprims(self._h, n))
+        return n
 
     def set_concurrent(self, on: bool = True) -> "Engine":
         """Class launches on 4 streams (default) or serialised on one."""

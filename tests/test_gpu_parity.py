@@ -39,6 +39,20 @@ def test_boys_device_vs_reference(gpu):
             assert np.allclose(row, ref, rtol=2e-14, atol=1e-300), (m, t, row, ref)
 
 
+def test_boys_device_uniform_warps(gpu):
+    """The warp-uniform Boys branches (every lane T < 40, every lane T >= 40)
+    give the same values as the reference (boys.hpp:23-44) as the mixed one."""
+    from paper_2412_13203_b200.eritile import Engine
+    e = Engine(0)
+    o = Oracle("orc")
+    rng = np.random.default_rng(4)
+    for Ts in (rng.uniform(0.0, 39.99, 64), rng.uniform(40.0, 120.0, 64), np.linspace(0.0, 80.0, 64)):
+        for m in range(0, 17):
+            F = e.boys(m, Ts)
+            for t, row in zip(Ts, F):
+                assert np.allclose(row, o.boys(m, float(t)), rtol=2e-14, atol=1e-300), (m, t)
+
+
 @pytest.mark.parametrize("mol,basis", [("water", "sto-3g"), ("water", "cc-pvdz"), ("benzene", "6-31g*")])
 def test_eri_quartets_all_classes(gpu, mol, basis):
     xyz, bas = geom(mol), BASIS[basis]
