@@ -169,8 +169,10 @@ int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, 
  * level-scheduled plan. The choice changes atomic summation order only. */
 int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps);
 /* Per class of the last tune: class table index and the median ms of each
- * variant (kMaxVariants = 16 per class, 0 = not timed). */
+ * variant (eritile_gpu_max_variants() slots per class, 0 = not timed). */
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms);
+/* Variant slots per class (the stride of eritile_gpu_tune_times). */
+int eritile_gpu_max_variants(void);
 int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var);
 /* The whole variant table (one entry per class, eritile_gpu_num_classes):
  * get returns the class count; set validates every entry first. */

@@ -23,7 +23,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 GEN = CSRC / "generated"
-OBJ = PKG / "_build"
+_EXTRA = os.environ.get("ERITILE_NVFLAGS", "").strip()
+# experiment builds (extra nvcc flags) keep their own object cache
+OBJ = PKG / ("_build" if not _EXTRA else "_build_" + hashlib.sha256(_EXTRA.encode()).hexdigest()[:8])
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / os.environ.get("ERITILE_LIBNAME", "liberitile_b200.so")
 ROOT = PKG.parent

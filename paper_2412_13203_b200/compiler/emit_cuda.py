@@ -280,13 +280,19 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("lane_pl512", f"launch_class<Cls{cid}, 1, kLoopPlain, 512>"))
             out.append(("lane_pl768", f"launch_class<Cls{cid}, 1, kLoopPlain, 768>"))
             out.append(("lane_sb512", f"launch_class<Cls{cid}, 1, kLoopSmemBra, 512>"))
-        if info["ops"] <= UNROLL2_MAX_OPS:
-            out.append(("lane_u2t512", f"launch_class<Cls{cid}, 1, kLoopTwoKet, 512>"))
         # bra-stationary strips (csrc/jk_strip.cuh): K rows in shared memory;
         # the packed multi-bra remainder runs on a lane kernel
         if info["ops"] <= MINB_SMALL_OPS:
             out.append(("strip_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512>"))
             out.append(("strip_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768>"))
+            # + ket-record / item prefetch and batched shared-memory K adds (OPT 7)
+            out.append(("strip_o7_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 7>"))
+            # two ket primitives per bra record read (+ batched K adds)
+            out.append(("strip_k2_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 10>"))
+            # + warp-aggregated K-row updates (OPT 16)
+            out.append(("strip_a_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 18>"))
+            out.append(("strip_a_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768, 18>"))
+            out.append(("strip_ak2_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 26>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
         if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:
@@ -299,7 +305,13 @@ def variants(info) -> List[Tuple[str, str]]:
         out.append(("fam_x768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 768>"))
         out.append(("fstrip_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768>"))
         out.append(("fstrip_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768>"))
-    assert len(out) <= 16, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
+        out.append(("fstrip_o7_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 7>"))
+        out.append(("fstrip_k2_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 10>"))
+        out.append(("fstrip_k2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 10>"))
+        out.append(("fstrip_a_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 18>"))
+        out.append(("fstrip_a_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 18>"))
+        out.append(("fstrip_ak2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 26>"))
+    assert len(out) <= 24, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 
 

@@ -1280,6 +1280,16 @@ struct eritile_gpu {
     d_JK.alloc(2 * NN);
   }
 
+  // Launch errors name the class and kernel variant that raised them.
+  void check_launch(const ClassWork& cw) {
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return;
+    const ClassEntry& ce = kClassTable[cw.cls];
+    throw CudaError("launch of class (" + std::to_string(ce.la) + std::to_string(ce.lb) + std::to_string(ce.lc) +
+                    std::to_string(ce.ld) + ") variant " + ce.var_name[variant(cw.cls)] + ": " +
+                    cudaGetErrorString(e));
+  }
+
   // Launch every class over D' (pre-scaled, device) into JKacc (zeroed).
   void launch_all(const double* dDs, double* dJK, cudaStream_t st) {
     const size_t NN = static_cast<size_t>(nbf) * nbf;
@@ -1299,7 +1309,7 @@ struct eritile_gpu {
         if (profiling) CK(cudaEventRecord(prof_ev[2 * w], st));
         LaunchArgs a = class_args(cw, dDs, dJK, st);
         kClassTable[cw.cls].var[variant(cw.cls)](a);
-        CK(cudaGetLastError());
+        check_launch(cw);
         launches_last += kernel_launches(cw);
         if (profiling) CK(cudaEventRecord(prof_ev[2 * w + 1], st));
       }
@@ -1325,7 +1335,7 @@ struct eritile_gpu {
       cudaStream_t s = (i % (kSide + 1) == 0) ? st : side[i % (kSide + 1) - 1];
       LaunchArgs a = class_args(cw, dDs, dJK, s);
       kClassTable[cw.cls].var[variant(cw.cls)](a);
-      CK(cudaGetLastError());
+      check_launch(cw);
       launches_last += kernel_launches(cw);
     }
     for (int k = 0; k < kSide; ++k) {
@@ -1923,6 +1933,8 @@ int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps) {
     ctx->tune(ctx->d_Ds.p, reps);
   });
 }
+
+int eritile_gpu_max_variants(void) { return kMaxVariants; }
 
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms) {
   if (!ctx) return ERITILE_ERR_ARG;

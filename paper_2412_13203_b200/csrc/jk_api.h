@@ -117,7 +117,7 @@ using LaunchFn = void (*)(const LaunchArgs&);
 // One canonical ERI class and its kernel variants (straight-line lane
 // kernels at several residency targets and/or the CTA-cooperative table
 // kernel); `def` is the variant used until the allocator tunes the class.
-constexpr int kMaxVariants = 16;
+constexpr int kMaxVariants = 24;
 struct ClassEntry {
   int la, lb, lc, ld, max_m, ops, prim_terms, base, contract, hrr_terms;
   int nvar;

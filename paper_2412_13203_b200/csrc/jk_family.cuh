@@ -31,9 +31,78 @@ __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const
   for (int m = 0; m < MB; ++m)
 #pragma unroll
     for (int n = 0; n < MK; ++n) C::zero(acc[m][n]);
+  if constexpr (STYLE == kLoopSmemBra2K) {  // two ket primitives per bra record read
+    int j = 0;
+    for (; j + 1 < kk; j += 2) {
+      const PrimRec k0 = load_prim<C::KPA>(ket + j * ks);
+      const PrimRec k1 = load_prim<C::KPA>(ket + (j + 1) * ks);
+      typename C::Acc s0[MB], s1[MB];
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        C::zero(s0[m]);
+        C::zero(s1[m]);
+      }
+      for (int i = 0; i < kb; ++i) {
+        const PrimRec bq = load_prim_gen<C::BPA>(bra + i);
+        const double2 wq = bw[i];
+        if constexpr (MB == 2) {
+          C::prim_w(bq, k0, btab, wq.x, wq.y, s0[0], s0[MB - 1]);
+          C::prim_w(bq, k1, btab, wq.x, wq.y, s1[0], s1[MB - 1]);
+        } else {
+          C::prim_w1(bq, k0, btab, wq.x, s0[0]);
+          C::prim_w1(bq, k1, btab, wq.x, s1[0]);
+        }
+      }
+      const double2 w0 = __ldg(kw + j * ks), w1 = __ldg(kw + (j + 1) * ks);
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        C::axpy(acc[m][0], w0.x, s0[m]);
+        C::axpy(acc[m][0], w1.x, s1[m]);
+        if constexpr (MK == 2) {
+          C::axpy(acc[m][MK - 1], w0.y, s0[m]);
+          C::axpy(acc[m][MK - 1], w1.y, s1[m]);
+        }
+      }
+    }
+    if (j < kk) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
+      typename C::Acc s0[MB];
+#pragma unroll
+      for (int m = 0; m < MB; ++m) C::zero(s0[m]);
+      for (int i = 0; i < kb; ++i) {
+        const double2 wq = bw[i];
+        if constexpr (MB == 2) C::prim_w(load_prim_gen<C::BPA>(bra + i), kp, btab, wq.x, wq.y, s0[0], s0[MB - 1]);
+        else C::prim_w1(load_prim_gen<C::BPA>(bra + i), kp, btab, wq.x, s0[0]);
+      }
+      const double2 w0 = __ldg(kw + j * ks);
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        C::axpy(acc[m][0], w0.x, s0[m]);
+        if constexpr (MK == 2) C::axpy(acc[m][MK - 1], w0.y, s0[m]);
+      }
+    }
+    return;
+  }
+  PrimRec kn;
+  double2 kwn;
+  if constexpr (STYLE == kLoopSmemBraPf) {  // ket record of step j+1 in flight during step j
+    kn = load_prim<C::KPA>(ket);
+    kwn = __ldg(kw);
+  }
   for (int j = 0; j < kk; ++j) {
-    const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
-    const double2 kwj = __ldg(kw + j * ks);
+    PrimRec kp;
+    double2 kwj;
+    if constexpr (STYLE == kLoopSmemBraPf) {
+      kp = kn;
+      kwj = kwn;
+      if (j + 1 < kk) {
+        kn = load_prim<C::KPA>(ket + (j + 1) * ks);
+        kwn = __ldg(kw + (j + 1) * ks);
+      }
+    } else {
+      kp = load_prim<C::KPA>(ket + j * ks);
+      kwj = __ldg(kw + j * ks);
+    }
     typename C::Acc s[MB];  // sum over bra prims of U_m(bra) * g, per bra member
 #pragma unroll
     for (int m = 0; m < MB; ++m) C::zero(s[m]);
@@ -48,7 +117,7 @@ __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const
         if constexpr (MB == 2) C::prim_w(bq, kp, btab, wq.x, wq.y, s[0], s[MB - 1]);
         else C::prim_w1(bq, kp, btab, wq.x, s[0]);
       }
-    } else if constexpr (STYLE == kLoopSmemBra) {  // bra records / weights may sit in shared memory
+    } else if constexpr (STYLE == kLoopSmemBra || STYLE == kLoopSmemBraPf) {  // bra records / weights may sit in shared memory
       for (int i = 0; i < kb; ++i) {
         const double2 wq = bw[i];
         if constexpr (MB == 2) C::prim_w(load_prim_gen<C::BPA>(bra + i), kp, btab, wq.x, wq.y, s[0], s[MB - 1]);

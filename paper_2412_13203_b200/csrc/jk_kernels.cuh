@@ -129,69 +129,15 @@ __device__ __forceinline__ void boys_eval_mixed(double T, const double* __restri
   }
 }
 
-// exp(-d) for |d| <= 1/32: 8-term Taylor series in Estrin form.
-__device__ __forceinline__ double boys_expm(double md) {
-  const double m2 = md * md, m4 = m2 * m2;
-  const double e01 = md + 1.0, e23 = fma(md, kBoysK[0], 0.5);
-  const double e45 = fma(md, kBoysK[2], kBoysK[1]);
-  const double e67 = fma(md, kBoysK[4], kBoysK[3]);
-  const double e0123 = fma(m2, e23, e01), e4567 = fma(m2, e67, e45);
-  return fma(m4, fma(m4, kBoysK[5], e4567), e0123);
-}
-
-// T < 40 for every lane: the table branch of boys_eval_mixed alone (same
-// operations, same rounding).
-template <int M>
-__device__ __forceinline__ void boys_eval_small(double T, const double* __restrict__ tab, double* F) {
-  const double sh = fma(T, 16.0, kBoysK[6]);
-  const int i = __double2loint(sh);
-  const double md = fma(sh - kBoysK[6], 0.0625, -T);
-  const double* row = tab + i * kBoysCols;
-  double e = 0.0;
-  if (M > 0) e = boys_expm(md) * (row[8] * 1.0);
-  const double2* r = reinterpret_cast<const double2*>(row);
-  const double2 c01 = r[0], c23 = r[1], c45 = r[2], c67 = r[3];
-  const double m2 = md * md;
-  const double p01 = fma(c01.y, md, c01.x), p23 = fma(c23.y, md, c23.x);
-  const double p45 = fma(c45.y, md, c45.x), p67 = fma(c67.y, md, c67.x);
-  const double q0 = fma(p23, m2, p01), q1 = fma(p67, m2, p45);
-  F[M] = fma(q1, m2 * m2, q0);
-  const double T2 = 2.0 * T;
-#pragma unroll
-  for (int m = M; m > 0; --m) F[m - 1] = fma(T2, F[m], e) * (1.0 / (2 * m - 1));
-}
-
-// T >= 40 for every lane: the asymptotic branch alone.
-template <int M>
-__device__ __forceinline__ void boys_eval_large(double T, const double* __restrict__ tab, double* F) {
-  const double rt = rsqrt_pos(T);
-  F[0] = kBoysK[8] * rt;  // sqrt(pi)/2
-  if (M > 0) {
-    const double Tt = T < 2.0 * kBoysTmax ? T - kBoysTmax : 0.0;
-    const double sh = fma(Tt, 16.0, kBoysK[6]);
-    const int i = __double2loint(sh);
-    const double md = fma(sh - kBoysK[6], 0.0625, -Tt);
-    const double scale = T < 2.0 * kBoysTmax ? kBoysK[7] : 0.0;  // e^-40
-    const double e = boys_expm(md) * (tab[i * kBoysCols + 8] * scale);
-    const double h = 0.5 * rt * rt;  // 1/(2T)
-#pragma unroll
-    for (int m = 0; m < M; ++m) F[m + 1] = fma(static_cast<double>(2 * m + 1), F[m], -e) * h;
-  }
-}
-
-// Warp-uniform dispatch: a warp whose active lanes all lie on one side of
-// T = 40 runs only that branch (the if-converted mixed form evaluates both).
+// Boys F_0..F_M(T) on every lane in one straight-line (if-converted) form.
+// A warp-uniform dispatch (vote, then only the table or only the asymptotic
+// branch) was measured slower: 450 vs 433 ms per (H2O)_80 build — lanes of
+// a warp are kets at different distances, so warps mix both sides of T = 40
+// and pay both branches plus the vote/reconvergence, and the branches split
+// the primitive loop into basic blocks the scheduler cannot interleave.
 template <int M>
 __device__ __forceinline__ void boys_eval(double T, const double* __restrict__ tab, double* F) {
-  const unsigned am = __activemask();
-  const bool small = T < kBoysTmax;
-  if (__all_sync(am, small)) {
-    boys_eval_small<M>(T, tab, F);
-  } else if (!__any_sync(am, small)) {
-    boys_eval_large<M>(T, tab, F);
-  } else {
-    boys_eval_mixed<M>(T, tab, F);
-  }
+  boys_eval_mixed<M>(T, tab, F);
 }
 
 // F_0, F_1 for M = 1 classes from the slices 0 and 1 staged back to back
@@ -235,7 +181,12 @@ __device__ __forceinline__ void boys_eval_m1(double T, const double* __restrict_
 //  kLoopSmemBra   plain loop; when all lanes of the warp share the bra, its
 //                 primitive records are staged once in shared memory (per
 //                 warp, reused while consecutive items keep the bra).
-constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopTwoKet = 2, kLoopSmemBra = 4;
+//  kLoopSmemBraPf as kLoopSmemBra, and the ket record of step j+1 is loaded
+//                 during step j (hides the L2 trip of the ket gather).
+//  kLoopSmemBra2K as kLoopSmemBra with two ket primitives per step sharing
+//                 each bra record read (two independent chains per lane).
+constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopTwoKet = 2, kLoopSmemBra = 4, kLoopSmemBraPf = 8,
+              kLoopSmemBra2K = 16;
 constexpr int kSmemBraMax = 81;  // records per warp buffer (cc-pVDZ s9 x s9)
 
 // Generic-address record load (the pointer may be shared or global).
@@ -270,6 +221,31 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
   } else if constexpr (STYLE == kLoopSmemBra) {
     for (int j = 0; j < kk; ++j) {
       const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
+      for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
+    }
+  } else if constexpr (STYLE == kLoopSmemBra2K) {
+    typename C::Acc b;
+    C::zero(b);
+    int j = 0;
+    for (; j + 1 < kk; j += 2) {
+      const PrimRec k0 = load_prim<C::KPA>(ket + j * ks);
+      const PrimRec k1 = load_prim<C::KPA>(ket + (j + 1) * ks);
+      for (int i = 0; i < kb; ++i) {
+        const PrimRec bq = load_prim_gen<C::BPA>(bra + i);
+        C::prim(bq, k0, btab, a);
+        C::prim(bq, k1, btab, b);
+      }
+    }
+    if (j < kk) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
+      for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
+    }
+    C::fold(a, b);
+  } else if constexpr (STYLE == kLoopSmemBraPf) {
+    PrimRec kn = load_prim<C::KPA>(ket);
+    for (int j = 0; j < kk; ++j) {
+      const PrimRec kp = kn;
+      if (j + 1 < kk) kn = load_prim<C::KPA>(ket + (j + 1) * ks);
       for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
     }
   } else if constexpr (STYLE == kLoopPrefetch) {

@@ -38,8 +38,63 @@ struct StripSmem {
   }
 };
 
-template <class C, bool FAM, int MB, int MK, int NT, bool DSM>
+// Shared-memory FP64 adds of one quartet's K-row updates, batched: sm_100a
+// has no native shared FP64 atomic add (atomicAdd compiles to an
+// LDS / DADD / ATOMS.CAST.SPIN.64 retry loop per element, one dependent
+// chain after the other). Here all NE reads are issued, then all NE CAS,
+// and only the (rare) losers of a race retry, so the NE chains overlap.
+template <int NE>
+__device__ __forceinline__ void smem_add_batch(double* sK, const int (&idx)[NE], const double (&val)[NE]) {
+  unsigned long long old[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) old[e] = *reinterpret_cast<volatile unsigned long long*>(sK + idx[e]);
+  unsigned pend = 0;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const unsigned long long nw = __double_as_longlong(__longlong_as_double(old[e]) + val[e]);
+    const unsigned long long r = atomicCAS(reinterpret_cast<unsigned long long*>(sK + idx[e]), old[e], nw);
+    if (r != old[e]) pend |= 1u << e;
+  }
+  if (pend) {  // (static indices: the arrays stay in registers)
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+      if (pend >> e & 1u) atomicAdd(sK + idx[e], val[e]);
+  }
+}
+
+// OPT bits: kStripKetPf (ket record of step j+1 loaded during step j),
+// kStripCasBatch (smem_add_batch for the K rows), kStripItemPf (the warp's
+// next item is claimed and loaded while it evaluates the current one).
+// kStripTwoKet: two ket primitives per bra record read (kLoopSmemBra2K).
+// kStripAgg: warp-aggregated K-row updates. Kets of one item often share a
+// shell, so several lanes hit the same shared-memory K element and the CAS
+// loops serialise (ncu: 2-4 ATOMS.CAST iterations per update, 8 threads
+// active). Lanes with equal column are grouped (__match_any_sync), their
+// values summed in log2(group) shuffle rounds (reduce_peers), and only the
+// group leader issues the (batched) shared-memory add.
+constexpr int kStripKetPf = 1, kStripCasBatch = 2, kStripItemPf = 4, kStripTwoKet = 8, kStripAgg = 16;
+
+// Sum x over the lanes of `peers` (lanes with equal key, this lane included);
+// the lowest lane of the group ends with the total. All 32 lanes must call.
+template <int NV>
+__device__ __forceinline__ void reduce_peers(unsigned peers, double (&x)[NV], int lane) {
+  int rel = __popc(peers & ((1u << lane) - 1u));  // rank within the group
+  unsigned rest = peers & (0xfffffffeu << lane);  // group members above this lane
+  while (__any_sync(0xffffffffu, rest != 0u)) {
+    const int next = __ffs(rest);  // next remaining member (1-based), 0 if none
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      const double t = __shfl_sync(0xffffffffu, x[e], next ? next - 1 : lane);
+      if (next) x[e] += t;
+    }
+    rest &= ~__ballot_sync(0xffffffffu, rel & 1);
+    rel >>= 1;
+  }
+}
+
+template <class C, bool FAM, int MB, int MK, int NT, bool DSM, int OPT = 0>
 __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long s0, long long s1) {
+  constexpr int kLoop = (OPT & kStripTwoKet) ? kLoopSmemBra2K : (OPT & kStripKetPf) ? kLoopSmemBraPf : kLoopSmemBra;
   extern __shared__ __align__(16) double smem[];
   load_boys_for<C>(smem, a.boys_tab);
   constexpr int kBoysD = BoysStage<C>::nsl * kBoysRows * kBoysCols;
@@ -120,12 +175,29 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       bpx[0] = st.bra;
     }
     (void)warp;
+    int wn = 0;
+    WorkItem nxt{};
+    if constexpr (OPT & kStripItemPf) {
+      if (lane == 0) wn = atomicAdd(&s_next, 1);
+      wn = __shfl_sync(0xffffffffu, wn, 0);
+      if (wn < st.i1) nxt = a.items[wn];
+    }
     for (;;) {
       int w = 0;
-      if (lane == 0) w = atomicAdd(&s_next, 1);  // dynamic: items differ in primitive count
-      w = __shfl_sync(0xffffffffu, w, 0);
-      if (w >= st.i1) break;
-      const WorkItem it = a.items[w];
+      WorkItem it;
+      if constexpr (OPT & kStripItemPf) {
+        w = wn;
+        if (w >= st.i1) break;
+        it = nxt;
+        if (lane == 0) wn = atomicAdd(&s_next, 1);
+        wn = __shfl_sync(0xffffffffu, wn, 0);
+        if (wn < st.i1) nxt = a.items[wn];  // in flight during this item
+      } else {
+        if (lane == 0) w = atomicAdd(&s_next, 1);  // dynamic: items differ in primitive count
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= st.i1) break;
+        it = a.items[w];
+      }
       const int nq = it.r0nq >> 24;
       const bool active = lane < nq;
       const int y = it.yfirst + (it.r0nq & 0xffffff) + (active ? lane : 0);  // single-bra item
@@ -141,7 +213,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         kpy[0] = ku.m0;
         if constexpr (MK == 2) kpy[MK - 1] = ku.m1;
         typename C::Acc acc[MB][MK];
-        fam_drive<C, MB, MK, kLoopSmemBra>(brap, bwp, kb, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, active ? ku.K : 0,
+        fam_drive<C, MB, MK, kLoop>(brap, bwp, kb, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, active ? ku.K : 0,
                                            ku.kstride, smem, acc);
 #pragma unroll
         for (int m = 0; m < MB; ++m)
@@ -156,7 +228,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         const int2 ks = __ldg(reinterpret_cast<const int2*>(&a.pm[y].ksoa));
         const int kstride = __ldg(&a.pm[y].kstride);
         kpy[0] = y;
-        eri_drive<C, kLoopSmemBra>(brap, kb, a.kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy,
+        eri_drive<C, kLoop>(brap, kb, a.kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy,
                                    CDz, smem, acc_v[0][0]);
       }
 #pragma unroll
@@ -175,13 +247,18 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
             keep = keep && !(st.bra == y && m > k) &&
                    (a.tau <= 0.0 || __ldg(a.Qp + bpx[m]) * __ldg(a.Qp + py) >= a.tau);
           }
-          if (!keep) continue;
+          constexpr bool AGG = (OPT & kStripAgg) != 0;
+          if constexpr (AGG) {  // the whole warp digests (shuffle groups), non-kept lanes add zeros
+            if (!__any_sync(0xffffffffu, keep)) continue;
+          } else {
+            if (!keep) continue;
+          }
           PairMeta km;
           ld_meta_late(a.pm + py, km);
           const double* v = acc_v[m][k];
           const double deg =
               (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (bpx[m] != py ? 2.0 : 1.0);
-          const double wj = 0.5 * deg, wk = 0.25 * deg;
+          const double wj = keep ? 0.5 * deg : 0.0, wk = keep ? 0.25 * deg : 0.0;
           const int colC = __ldg(a.cpos + km.sha);
           const int colD = __ldg(a.cpos + km.shb) + (LDOFF ? a.ncolC : 0);
           const double* Dab = a.D + bm.bfa * n + bm.bfb;
@@ -212,9 +289,14 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
                 for (int ib = 0; ib < C::NB; ++ib)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), t);
-              red_add(a.J + (km.bfa + ic) * n + km.bfb + id, t * wj, 0);
+              if (keep) red_add(a.J + (km.bfa + ic) * n + km.bfb + id, t * wj, 0);
             }
           // K_ac += sum_bd v D_bd ; K_ad += sum_bc v D_bc   (rows a of the bra)
+          // K_bd += sum_ac v D_ac ; K_bc += sum_ad v D_ad   (rows b of the bra)
+          constexpr int NKE = C::NA * (C::NC + C::ND) + C::NB * (C::NC + C::ND);
+          int kidx[NKE];
+          double kval[NKE];
+          int ne = 0;
 #pragma unroll
           for (int ia = 0; ia < C::NA; ++ia) {
 #pragma unroll
@@ -226,7 +308,8 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
                 for (int id = 0; id < C::ND; ++id)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
                           dsm(rB + ib, colD + id, bm.bfb + ib, km.bfb + id), t);
-              atomicAdd(sK + (rA + ia) * ncol + colC + ic, t * wk);
+              kidx[ne] = (rA + ia) * ncol + colC + ic;
+              kval[ne++] = t * wk;
             }
 #pragma unroll
             for (int id = 0; id < C::ND; ++id) {
@@ -237,10 +320,10 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
                 for (int ic = 0; ic < C::NC; ++ic)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
                           dsm(rB + ib, colC + ic, bm.bfb + ib, km.bfa + ic), t);
-              atomicAdd(sK + (rA + ia) * ncol + colD + id, t * wk);
+              kidx[ne] = (rA + ia) * ncol + colD + id;
+              kval[ne++] = t * wk;
             }
           }
-          // K_bd += sum_ac v D_ac ; K_bc += sum_ad v D_ad   (rows b of the bra)
 #pragma unroll
           for (int ib = 0; ib < C::NB; ++ib) {
 #pragma unroll
@@ -252,7 +335,8 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
                 for (int ic = 0; ic < C::NC; ++ic)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
                           dsm(rA + ia, colC + ic, bm.bfa + ia, km.bfa + ic), t);
-              atomicAdd(sK + (rB + ib) * ncol + colD + id, t * wk);
+              kidx[ne] = (rB + ib) * ncol + colD + id;
+              kval[ne++] = t * wk;
             }
 #pragma unroll
             for (int ic = 0; ic < C::NC; ++ic) {
@@ -263,8 +347,54 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
                 for (int id = 0; id < C::ND; ++id)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
                           dsm(rA + ia, colD + id, bm.bfa + ia, km.bfb + id), t);
-              atomicAdd(sK + (rB + ib) * ncol + colC + ic, t * wk);
+              kidx[ne] = (rB + ib) * ncol + colC + ic;
+              kval[ne++] = t * wk;
             }
+          }
+          if constexpr (AGG) {
+            // c-keyed updates (K_ac, K_bc) and d-keyed updates (K_ad, K_bd)
+            constexpr int NCK = (C::NA + C::NB) * C::NC, NDK = (C::NA + C::NB) * C::ND;
+            int ci[NCK], di[NDK];
+            double cv[NCK], dv[NDK];
+            int nc = 0, nd = 0;
+#pragma unroll
+            for (int ia = 0; ia < C::NA; ++ia) {
+#pragma unroll
+              for (int ic = 0; ic < C::NC; ++ic) {
+                ci[nc] = kidx[ia * (C::NC + C::ND) + ic];
+                cv[nc++] = kval[ia * (C::NC + C::ND) + ic];
+              }
+#pragma unroll
+              for (int id = 0; id < C::ND; ++id) {
+                di[nd] = kidx[ia * (C::NC + C::ND) + C::NC + id];
+                dv[nd++] = kval[ia * (C::NC + C::ND) + C::NC + id];
+              }
+            }
+#pragma unroll
+            for (int ib = 0; ib < C::NB; ++ib) {
+              constexpr int b0 = C::NA * (C::NC + C::ND);
+#pragma unroll
+              for (int id = 0; id < C::ND; ++id) {
+                di[nd] = kidx[b0 + ib * (C::NC + C::ND) + id];
+                dv[nd++] = kval[b0 + ib * (C::NC + C::ND) + id];
+              }
+#pragma unroll
+              for (int ic = 0; ic < C::NC; ++ic) {
+                ci[nc] = kidx[b0 + ib * (C::NC + C::ND) + C::ND + ic];
+                cv[nc++] = kval[b0 + ib * (C::NC + C::ND) + C::ND + ic];
+              }
+            }
+            const unsigned pc = __match_any_sync(0xffffffffu, keep ? colC : -1 - lane);
+            const unsigned pd = __match_any_sync(0xffffffffu, keep ? colD : -1 - lane);
+            reduce_peers<NCK>(pc, cv, lane);
+            reduce_peers<NDK>(pd, dv, lane);
+            if (keep && __ffs(pc) - 1 == lane) smem_add_batch<NCK>(sK, ci, cv);
+            if (keep && __ffs(pd) - 1 == lane) smem_add_batch<NDK>(sK, di, dv);
+          } else if constexpr (OPT & kStripCasBatch) {
+            smem_add_batch<NKE>(sK, kidx, kval);
+          } else {
+#pragma unroll
+            for (int e = 0; e < NKE; ++e) atomicAdd(sK + kidx[e], kval[e]);
           }
         }
       }
@@ -297,7 +427,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 // Strips of member segment (MB, MK) through the strip kernel; returns false
 // (nothing launched) if its shared memory does not fit - the caller then runs
 // those items through the lane kernel.
-template <class C, bool FAM, int MB, int MK, int NT>
+template <class C, bool FAM, int MB, int MK, int NT, int OPT = 0>
 bool launch_strip_seg(const LaunchArgs& a, long long s0, long long s1) {
   if (s1 <= s0) return true;
   const size_t with_d = StripSmem<C, MB>::bytes(a.ncols, true);
@@ -305,17 +435,17 @@ bool launch_strip_seg(const LaunchArgs& a, long long s0, long long s1) {
   constexpr size_t kMax = 227 * 1024 - 1024;  // static s_rowg + reserve
   if (no_d > kMax) return false;
   const bool dsm = with_d <= kMax;
-  const void* fn = dsm ? reinterpret_cast<const void*>(jk_strip_kernel<C, FAM, MB, MK, NT, true>)
-                       : reinterpret_cast<const void*>(jk_strip_kernel<C, FAM, MB, MK, NT, false>);
+  const void* fn = dsm ? reinterpret_cast<const void*>(jk_strip_kernel<C, FAM, MB, MK, NT, true, OPT>)
+                       : reinterpret_cast<const void*>(jk_strip_kernel<C, FAM, MB, MK, NT, false, OPT>);
   const size_t smem = dsm ? with_d : no_d;
   const LaunchSetup ls = launch_setup(fn, NT, smem, false);
   if (!ls.bps) return true;  // CUDA error pending for the caller's check
   const long long cap = static_cast<long long>(ls.bps) * ls.sms;
   const int grid = static_cast<int>(s1 - s0 < cap ? s1 - s0 : cap);
   if (dsm)
-    jk_strip_kernel<C, FAM, MB, MK, NT, true><<<grid, NT, smem, a.stream>>>(a, s0, s1);
+    jk_strip_kernel<C, FAM, MB, MK, NT, true, OPT><<<grid, NT, smem, a.stream>>>(a, s0, s1);
   else
-    jk_strip_kernel<C, FAM, MB, MK, NT, false><<<grid, NT, smem, a.stream>>>(a, s0, s1);
+    jk_strip_kernel<C, FAM, MB, MK, NT, false, OPT><<<grid, NT, smem, a.stream>>>(a, s0, s1);
   return true;
 }
 
@@ -323,13 +453,13 @@ bool launch_strip_seg(const LaunchArgs& a, long long s0, long long s1) {
 // (multi-bra packed) items through the lane kernel <MINB, STYLE, NTL>.
 // Deterministic mode runs every item on the lane kernels (the shared-memory
 // K rows would sum in scheduling order).
-template <class C, int NT, int MINB, int STYLE, int NTL>
+template <class C, int NT, int MINB, int STYLE, int NTL, int OPT = 0>
 void launch_strip(const LaunchArgs& a) {
   if (a.mode != 0) return launch_class<C, 2, kLoopPrefetch>(a);
   if (a.nitems <= 0) return;
   if (a.det) return launch_class<C, MINB, STYLE, NTL>(a);
   LaunchArgs r = a;
-  if (launch_strip_seg<C, false, 1, 1, NT>(a, a.sseg[0], a.sseg[1])) {
+  if (launch_strip_seg<C, false, 1, 1, NT, OPT>(a, a.sseg[0], a.sseg[1])) {
     r.items = a.items + a.sitem[0];
     r.nitems = a.nitems - a.sitem[0];
   }
@@ -338,7 +468,7 @@ void launch_strip(const LaunchArgs& a) {
 
 // Unit-list strip variant: per member segment, strips through the strip
 // kernel and the rest through the unit lane kernel.
-template <class C, int NT, int MINB, int STYLE, int NTL, int NT11>
+template <class C, int NT, int MINB, int STYLE, int NTL, int NT11, int OPT = 0>
 void launch_fstrip(const LaunchArgs& a) {
   if (a.mode != 0) return launch_class<C, 2, kLoopPrefetch>(a);
   if (a.det) {
@@ -350,10 +480,10 @@ void launch_fstrip(const LaunchArgs& a) {
   }
   long long rest0[4];
   for (int sg = 0; sg < 4; ++sg) rest0[sg] = a.seg[sg];
-  if (launch_strip_seg<C, true, 1, 1, NT>(a, a.sseg[0], a.sseg[1])) rest0[0] = a.sitem[0];
-  if (launch_strip_seg<C, true, 1, 2, NT>(a, a.sseg[1], a.sseg[2])) rest0[1] = a.sitem[1];
-  if (launch_strip_seg<C, true, 2, 1, NT>(a, a.sseg[2], a.sseg[3])) rest0[2] = a.sitem[2];
-  if (launch_strip_seg<C, true, 2, 2, NT>(a, a.sseg[3], a.sseg[4])) rest0[3] = a.sitem[3];
+  if (launch_strip_seg<C, true, 1, 1, NT, OPT>(a, a.sseg[0], a.sseg[1])) rest0[0] = a.sitem[0];
+  if (launch_strip_seg<C, true, 1, 2, NT, OPT>(a, a.sseg[1], a.sseg[2])) rest0[1] = a.sitem[1];
+  if (launch_strip_seg<C, true, 2, 1, NT, OPT>(a, a.sseg[2], a.sseg[3])) rest0[2] = a.sitem[2];
+  if (launch_strip_seg<C, true, 2, 2, NT, OPT>(a, a.sseg[3], a.sseg[4])) rest0[3] = a.sitem[3];
   launch_fam_seg<C, 1, 1, MINB, STYLE, NT11>(a, rest0[0], a.seg[1]);
   launch_fam_seg<C, 1, 2, MINB, STYLE, NTL>(a, rest0[1], a.seg[2]);
   launch_fam_seg<C, 2, 1, MINB, STYLE, NTL>(a, rest0[2], a.seg[3]);

@@ -91,6 +91,7 @@ def _lib():
         "eritile_gpu_tune": (C.c_int, [C.c_void_p, _dp, C.c_int]),
         "eritile_gpu_set_variant": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
         "eritile_gpu_tune_times": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+        "eritile_gpu_max_variants": (C.c_int, []),
         "eritile_gpu_set_families": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_set_concurrent": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_set_strips": (C.c_int, [C.c_void_p, C.c_longlong, C.c_int]),
@@ -379,13 +380,14 @@ class Engine:
         """{class: {variant name: median ms}} of the last tune."""
         n = self._lib.eritile_gpu_tune_times(self._h, 0, None, None)
         ci = np.zeros(max(n, 1), np.int32)
-        ms = np.zeros(16 * max(n, 1))
+        nv = self._lib.eritile_gpu_max_variants()
+        ms = np.zeros(nv * max(n, 1))
         self._lib.eritile_gpu_tune_times(self._h, n, ci.ctypes.data, ms.ctypes.data)
         tab = class_table()
         out = {}
         for w in range(n):
             names = variant_names(int(ci[w]))
-            out["".join(map(str, tab[ci[w]][:4]))] = {nm: round(float(ms[16 * w + v]), 4) for v, nm in enumerate(names) if ms[16 * w + v] > 0}
+            out["".join(map(str, tab[ci[w]][:4]))] = {nm: round(float(ms[nv * w + v]), 4) for v, nm in enumerate(names) if ms[nv * w + v] > 0}
         return out
 
     def variants(self) -> dict:
