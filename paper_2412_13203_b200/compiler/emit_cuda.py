@@ -288,11 +288,16 @@ def variants(info) -> List[Tuple[str, str]]:
             # + ket-record / item prefetch and batched shared-memory K adds (OPT 7)
             out.append(("strip_o7_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 7>"))
             # two ket primitives per bra record read (+ batched K adds)
-            out.append(("strip_k2_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 10>"))
             # + warp-aggregated K-row updates (OPT 16)
             out.append(("strip_a_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 18>"))
             out.append(("strip_a_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768, 18>"))
             out.append(("strip_ak2_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 26>"))
+            # + L1 prefetch of the next ket record / next item's metadata (OPT 32|4)
+            out.append(("strip_p_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 54>"))
+            out.append(("strip_p_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768, 54>"))
+            # + d-column K updates to global memory (OPT 64)
+            out.append(("strip_s_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 82>"))
+            out.append(("strip_s_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768, 82>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
         if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:
@@ -306,12 +311,16 @@ def variants(info) -> List[Tuple[str, str]]:
         out.append(("fstrip_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768>"))
         out.append(("fstrip_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768>"))
         out.append(("fstrip_o7_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 7>"))
-        out.append(("fstrip_k2_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 10>"))
         out.append(("fstrip_k2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 10>"))
         out.append(("fstrip_a_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 18>"))
         out.append(("fstrip_a_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 18>"))
         out.append(("fstrip_ak2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 26>"))
-    assert len(out) <= 24, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
+        out.append(("fstrip_p_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 54>"))
+        out.append(("fstrip_p_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 54>"))
+        out.append(("fstrip_s_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 82>"))
+        out.append(("fstrip_s_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 82>"))
+        out.append(("fstrip_sk2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 90>"))
+    assert len(out) <= 32, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 
 

@@ -294,6 +294,7 @@ struct eritile_gpu {
   std::vector<PrimRec> ukprims;
   std::vector<double2> ukw;
   DevBuf<UnitMeta> d_um;
+  DevBuf<KetMeta> d_kmu, d_kmp;  // KetMeta per unit / per product pair
   DevBuf<double2> d_uw, d_ukw;
   DevBuf<PrimRec> d_ukprims;
   DevBuf<double> d_Qp;
@@ -450,6 +451,7 @@ struct eritile_gpu {
       a.ncolC = cols_nc[ce.lc][ce.ld];
       a.cpos = d_cpos.p;
     }
+    a.kmeta = cw.fam ? d_kmu.p : d_kmp.p;
     if (cw.fam) {
       a.um = d_um.p;
       a.uw = d_uw.p;
@@ -841,6 +843,41 @@ struct eritile_gpu {
     }
   }
 
+  // KetMeta of product pair x (both member slots) / of unit u.
+  KetMeta ket_meta_pair(int x) const {
+    KetMeta k{};
+    for (int s = 0; s < 2; ++s) {
+      k.bfa[s] = pm[x].bfa;
+      k.bfb[s] = pm[x].bfb;
+      k.colc[s] = shell_cpos[pm[x].sha];
+      k.cold[s] = shell_cpos[pm[x].shb];
+      k.offd[s] = pm[x].sha != pm[x].shb;
+      k.m[s] = x;
+      k.q[s] = Q.empty() ? 0.0 : Q[x];
+    }
+    return k;
+  }
+  void build_ket_meta(bool units) {
+    if (host_only) return;
+    std::vector<KetMeta> kp(pm.size());
+    for (size_t x = 0; x < pm.size(); ++x) kp[x] = ket_meta_pair(static_cast<int>(x));
+    d_kmp.upload(kp, stream);
+    if (!units) return;
+    std::vector<KetMeta> ku(um.size());
+    for (size_t u = 0; u < um.size(); ++u) {
+      const KetMeta a = ket_meta_pair(um[u].m0), b = ket_meta_pair(um[u].m1);
+      ku[u] = a;
+      ku[u].bfa[1] = b.bfa[1];
+      ku[u].bfb[1] = b.bfb[1];
+      ku[u].colc[1] = b.colc[1];
+      ku[u].cold[1] = b.cold[1];
+      ku[u].offd[1] = b.offd[1];
+      ku[u].m[1] = b.m[1];
+      ku[u].q[1] = b.q[1];
+    }
+    d_kmu.upload(ku, stream);
+  }
+
   // Member quartets of unit pair (u, v) that survive (Q_m Q_n >= tau) and
   // are canonical (u == v: members m <= n only).
   int unit_pair_quartets(int u, int v, double t) const {
@@ -865,6 +902,7 @@ struct eritile_gpu {
     bool any_fam = false;
     for (int c = 0; c < kNumClasses; ++c) any_fam = any_fam || fam_active(c);
     if (any_fam) build_units();
+    build_ket_meta(any_fam);
     // enumerate group pairs X >= Y (pair groups, or unit groups for classes
     // served by the shared-primitive kernels), grouped by angular class
     struct GP {
@@ -1065,14 +1103,24 @@ struct eritile_gpu {
       cw.aseg[4] = cw.an;
       cw.asseg[4] = static_cast<long long>(all_strips.size()) - cw.astrip_off;
       if (std::getenv("ERITILE_DEBUG_ITEMS") && cw.an > 0) {  // diagnostics: items spanning > 1 bra
-        long long multi = 0;
+        long long multi = 0, lanes = 0, slanes = 0, sitems = 0;
         for (long long w = cw.aoff; w < cw.aoff + cw.an; ++w) {
           const WorkItem& it = all_items[w];
           if ((it.r0nq & 0xffffff) + (it.r0nq >> 24) > cnt[it.cntp]) ++multi;
+          lanes += it.r0nq >> 24;
+          bool in_strip = false;
+          for (int sg = 0; sg < 4; ++sg)
+            if (w - cw.aoff >= cw.aseg[sg] && w - cw.aoff < cw.asitem[sg]) in_strip = true;
+          if (in_strip) {
+            ++sitems;
+            slanes += it.r0nq >> 24;
+          }
         }
-        std::fprintf(stderr, "class %d fam %d items %lld multi-bra %.3f strips %lld strip items %lld\n", cls,
-                     fam ? 1 : 0, cw.an, static_cast<double>(multi) / cw.an, cw.asseg[4],
-                     cw.asitem[0] + cw.asitem[1] - cw.aseg[1] + cw.asitem[2] - cw.aseg[2] + cw.asitem[3] - cw.aseg[3]);
+        std::fprintf(stderr,
+                     "class %d fam %d items %lld multi-bra %.3f strips %lld strip items %lld lane fill %.3f "
+                     "(strip items %.3f)\n",
+                     cls, fam ? 1 : 0, cw.an, static_cast<double>(multi) / cw.an, cw.asseg[4], sitems,
+                     lanes / (32.0 * cw.an), sitems ? slanes / (32.0 * sitems) : 0.0);
       }
       if (cw.an > 0) {
         const ClassEntry& ce = kClassTable[cls];

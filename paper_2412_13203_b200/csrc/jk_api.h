@@ -63,6 +63,17 @@ constexpr int kStripBraMax = 128;
 // of partial sums is harmless); rounding error <= 2^-45 per contribution.
 constexpr double kDetScale = 17592186044416.0;  // 2^44  // strip bras: primitive pairs staged in shared memory
 
+// Digestion metadata of a ket unit (or product pair: member 1 = member 0),
+// one 64-byte read per lane and item in the strip kernels instead of the
+// dependent PairMeta -> cpos chain after the primitive loop.
+struct alignas(16) KetMeta {
+  int bfa[2], bfb[2];    // first basis functions of member m's C / D shells
+  int colc[2], cold[2];  // compact column (cpos) of member m's C / D shells
+  int offd[2];           // 1 if member m's shells differ (sha != shb)
+  int m[2];              // product pair id of member m
+  double q[2];           // Schwarz Q of member m
+};
+
 struct alignas(16) Strip {
   int bra, i0, i1, nrows;
   int rowA[2], rowB[2];
@@ -109,6 +120,7 @@ struct LaunchArgs {
   int det;          // deterministic mode: J/K accumulate as int64 fixed point (kDetScale)
   const int* cols;  // compact K/D column list of the class: L_C functions (++ L_D functions if L_D != L_C)
   const int* cpos;  // per shell: first compact column within its own L list
+  const KetMeta* kmeta;  // per ket unit (unit kernels) or per product pair
   int ncols, ncolC;
 };
 
@@ -117,7 +129,7 @@ using LaunchFn = void (*)(const LaunchArgs&);
 // One canonical ERI class and its kernel variants (straight-line lane
 // kernels at several residency targets and/or the CTA-cooperative table
 // kernel); `def` is the variant used until the allocator tunes the class.
-constexpr int kMaxVariants = 24;
+constexpr int kMaxVariants = 32;
 struct ClassEntry {
   int la, lb, lc, ld, max_m, ops, prim_terms, base, contract, hrr_terms;
   int nvar;

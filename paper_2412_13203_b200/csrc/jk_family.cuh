@@ -100,6 +100,11 @@ __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const
         kwn = __ldg(kw + (j + 1) * ks);
       }
     } else {
+      if constexpr (STYLE == kLoopSmemBraL1)
+        if (j + 1 < kk) {
+          prefetch_l1(ket + (j + 1) * ks);
+          prefetch_l1(kw + (j + 1) * ks);
+        }
       kp = load_prim<C::KPA>(ket + j * ks);
       kwj = __ldg(kw + j * ks);
     }
@@ -117,7 +122,7 @@ __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const
         if constexpr (MB == 2) C::prim_w(bq, kp, btab, wq.x, wq.y, s[0], s[MB - 1]);
         else C::prim_w1(bq, kp, btab, wq.x, s[0]);
       }
-    } else if constexpr (STYLE == kLoopSmemBra || STYLE == kLoopSmemBraPf) {  // bra records / weights may sit in shared memory
+    } else if constexpr (STYLE == kLoopSmemBra || STYLE == kLoopSmemBraPf || STYLE == kLoopSmemBraL1) {  // bra records / weights may sit in shared memory
       for (int i = 0; i < kb; ++i) {
         const double2 wq = bw[i];
         if constexpr (MB == 2) C::prim_w(load_prim_gen<C::BPA>(bra + i), kp, btab, wq.x, wq.y, s[0], s[MB - 1]);

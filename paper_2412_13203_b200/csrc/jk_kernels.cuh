@@ -185,8 +185,15 @@ __device__ __forceinline__ void boys_eval_m1(double T, const double* __restrict_
 //                 during step j (hides the L2 trip of the ket gather).
 //  kLoopSmemBra2K as kLoopSmemBra with two ket primitives per step sharing
 //                 each bra record read (two independent chains per lane).
+//  kLoopSmemBraL1 as kLoopSmemBra, and step j issues an L1 prefetch of the
+//                 ket record of step j+1 (no registers held; ncu showed the
+//                 first use of each ket record as the top long-scoreboard stall).
 constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopTwoKet = 2, kLoopSmemBra = 4, kLoopSmemBraPf = 8,
-              kLoopSmemBra2K = 16;
+              kLoopSmemBra2K = 16, kLoopSmemBraL1 = 32;
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 constexpr int kSmemBraMax = 81;  // records per warp buffer (cc-pVDZ s9 x s9)
 
 // Generic-address record load (the pointer may be shared or global).
@@ -218,8 +225,10 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
       const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
       for (int i = 0; i < kb; ++i) C::prim(load_prim<C::BPA>(bra + i), kp, btab, a);
     }
-  } else if constexpr (STYLE == kLoopSmemBra) {
+  } else if constexpr (STYLE == kLoopSmemBra || STYLE == kLoopSmemBraL1) {
     for (int j = 0; j < kk; ++j) {
+      if constexpr (STYLE == kLoopSmemBraL1)
+        if (j + 1 < kk) prefetch_l1(ket + (j + 1) * ks);
       const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
       for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
     }

@@ -24,6 +24,9 @@
 // results differ from the other variants only by summation order.
 #pragma once
 #include "jk_family.cuh"
+#ifndef ERITILE_PROBE_STRIP
+#define ERITILE_PROBE_STRIP 0
+#endif
 
 namespace eritile_b200 {
 
@@ -72,7 +75,11 @@ __device__ __forceinline__ void smem_add_batch(double* sK, const int (&idx)[NE],
 // active). Lanes with equal column are grouped (__match_any_sync), their
 // values summed in log2(group) shuffle rounds (reduce_peers), and only the
 // group leader issues the (batched) shared-memory add.
-constexpr int kStripKetPf = 1, kStripCasBatch = 2, kStripItemPf = 4, kStripTwoKet = 8, kStripAgg = 16;
+// kStripL1Pf: L1 prefetch of the next ket record (kLoopSmemBraL1) and, with
+// kStripItemPf, of the next item's ket metadata and first ket record.
+// kStripSplitK (with kStripAgg): the d-column K updates go to global memory.
+constexpr int kStripKetPf = 1, kStripCasBatch = 2, kStripItemPf = 4, kStripTwoKet = 8, kStripAgg = 16,
+              kStripL1Pf = 32, kStripSplitK = 64;
 
 // Sum x over the lanes of `peers` (lanes with equal key, this lane included);
 // the lowest lane of the group ends with the total. All 32 lanes must call.
@@ -94,7 +101,10 @@ __device__ __forceinline__ void reduce_peers(unsigned peers, double (&x)[NV], in
 
 template <class C, bool FAM, int MB, int MK, int NT, bool DSM, int OPT = 0>
 __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long s0, long long s1) {
-  constexpr int kLoop = (OPT & kStripTwoKet) ? kLoopSmemBra2K : (OPT & kStripKetPf) ? kLoopSmemBraPf : kLoopSmemBra;
+  constexpr int kLoop = (OPT & kStripTwoKet)  ? kLoopSmemBra2K
+                        : (OPT & kStripKetPf) ? kLoopSmemBraPf
+                        : (OPT & kStripL1Pf)  ? kLoopSmemBraL1
+                                              : kLoopSmemBra;
   extern __shared__ __align__(16) double smem[];
   load_boys_for<C>(smem, a.boys_tab);
   constexpr int kBoysD = BoysStage<C>::nsl * kBoysRows * kBoysCols;
@@ -106,6 +116,8 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
   __shared__ int s_rowg[StripSmem<C, MB>::kRowsMax];  // global basis function of each smem row
   __shared__ int s_bm[MB][4];                         // bra members: bfa, bfb, sha, shb
   __shared__ int s_next;                              // next item of the strip (dynamic hand-out)
+  __shared__ double s_bq[MB];                         // Schwarz Q of the bra members
+  __shared__ double s_bab[3];                         // bra AB vector
   (void)sD;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
@@ -146,6 +158,14 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       s_bm[threadIdx.x][1] = bm.bfb;
       s_bm[threadIdx.x][2] = bm.sha;
       s_bm[threadIdx.x][3] = bm.shb;
+      s_bq[threadIdx.x] = FAM ? __ldg(a.Qp + px) : 0.0;
+    }
+    if (threadIdx.x == 32) {
+      if constexpr (FAM) {
+        s_bab[0] = a.um[st.bra].ABx; s_bab[1] = a.um[st.bra].ABy; s_bab[2] = a.um[st.bra].ABz;
+      } else {
+        s_bab[0] = a.pm[st.bra].ABx; s_bab[1] = a.pm[st.bra].ABy; s_bab[2] = a.pm[st.bra].ABz;
+      }
     }
     if (threadIdx.x == 0) s_next = st.i0;
     for (int e = threadIdx.x; e < nrows * ncol; e += NT) sK[e] = 0.0;
@@ -192,6 +212,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         if (lane == 0) wn = atomicAdd(&s_next, 1);
         wn = __shfl_sync(0xffffffffu, wn, 0);
         if (wn < st.i1) nxt = a.items[wn];  // in flight during this item
+
       } else {
         if (lane == 0) w = atomicAdd(&s_next, 1);  // dynamic: items differ in primitive count
         w = __shfl_sync(0xffffffffu, w, 0);
@@ -203,33 +224,69 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       const int y = it.yfirst + (it.r0nq & 0xffffff) + (active ? lane : 0);  // single-bra item
       double acc_v[MB][MK][C::NV];
       (void)acc_v;
-      int kpy[MK];
       double ABx, ABy, ABz, CDx, CDy, CDz;
       if constexpr (FAM) {
-        const UnitMeta bu = a.um[st.bra];
         const UnitMeta ku = a.um[y];
-        ABx = bu.ABx; ABy = bu.ABy; ABz = bu.ABz;
+        ABx = s_bab[0]; ABy = s_bab[1]; ABz = s_bab[2];
         CDx = ku.ABx; CDy = ku.ABy; CDz = ku.ABz;
-        kpy[0] = ku.m0;
-        if constexpr (MK == 2) kpy[MK - 1] = ku.m1;
         typename C::Acc acc[MB][MK];
+#if ERITILE_PROBE_STRIP == 2  // measurement build: no primitive loop
+        fam_drive<C, MB, MK, kLoop>(brap, bwp, kb, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, 0,
+#else
         fam_drive<C, MB, MK, kLoop>(brap, bwp, kb, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, active ? ku.K : 0,
+#endif
                                            ku.kstride, smem, acc);
 #pragma unroll
         for (int m = 0; m < MB; ++m)
 #pragma unroll
           for (int k = 0; k < MK; ++k) C::finish(acc[m][k], ABx, ABy, ABz, CDx, CDy, CDz, acc_v[m][k]);
       } else {
-        const PairMeta* bmp = a.pm + st.bra;
-        ABx = bmp->ABx; ABy = bmp->ABy; ABz = bmp->ABz;
+        ABx = s_bab[0]; ABy = s_bab[1]; ABz = s_bab[2];
         const int4 kh = __ldg(reinterpret_cast<const int4*>(a.pm + y));
         const double2 cd = __ldg(reinterpret_cast<const double2*>(&a.pm[y].ABx));
         CDx = cd.x; CDy = cd.y; CDz = __ldg(&a.pm[y].ABz);
         const int2 ks = __ldg(reinterpret_cast<const int2*>(&a.pm[y].ksoa));
         const int kstride = __ldg(&a.pm[y].kstride);
-        kpy[0] = y;
         eri_drive<C, kLoop>(brap, kb, a.kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy,
                                    CDz, smem, acc_v[0][0]);
+      }
+#if ERITILE_PROBE_STRIP == 1  // measurement build: no digestion (keep the integrals live)
+      {
+        double t = 0.0;
+#pragma unroll
+        for (int m = 0; m < MB; ++m)
+#pragma unroll
+          for (int k = 0; k < MK; ++k)
+#pragma unroll
+            for (int e = 0; e < C::NV; ++e) t += acc_v[m][k][e];
+        if (t == 1.2345e-300) a.J[lane] = t;
+        continue;
+      }
+#endif
+      if constexpr ((OPT & kStripL1Pf) && (OPT & kStripItemPf)) {
+        // the next item has arrived by now: warm L1 with its ket metadata
+        if (wn < st.i1) {
+          const int nqn = nxt.r0nq >> 24;
+          const int yn = nxt.yfirst + (nxt.r0nq & 0xffffff) + (lane < nqn ? lane : 0);
+          if constexpr (FAM) prefetch_l1(a.um + yn);
+          else prefetch_l1(a.pm + yn);
+        }
+      }
+      // digestion metadata of this lane's ket: one 64-byte read (no registers
+      // held across the primitive loop; measured slower when loaded up front)
+      KetMeta km;
+      {
+        const int4* kq = reinterpret_cast<const int4*>(a.kmeta + y);
+        int4 q0, q1, q2;
+        double2 q3;
+        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q0.x), "=r"(q0.y), "=r"(q0.z), "=r"(q0.w) : "l"(kq));
+        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q1.x), "=r"(q1.y), "=r"(q1.z), "=r"(q1.w) : "l"(kq + 1));
+        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q2.x), "=r"(q2.y), "=r"(q2.z), "=r"(q2.w) : "l"(kq + 2));
+        asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(q3.x), "=d"(q3.y) : "l"(kq + 3));
+        km.bfa[0] = q0.x; km.bfa[1] = q0.y; km.bfb[0] = q0.z; km.bfb[1] = q0.w;
+        km.colc[0] = q1.x; km.colc[1] = q1.y; km.cold[0] = q1.z; km.cold[1] = q1.w;
+        km.offd[0] = q2.x; km.offd[1] = q2.y; km.m[0] = q2.z; km.m[1] = q2.w;
+        km.q[0] = q3.x; km.q[1] = q3.y;
       }
 #pragma unroll
       for (int m = 0; m < MB; ++m) {
@@ -241,28 +298,24 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         const int rA = st.rowA[m], rB = st.rowB[m];
 #pragma unroll
         for (int k = 0; k < MK; ++k) {
-          const int py = kpy[k];
+          const int py = km.m[k];
           bool keep = active;
-          if constexpr (FAM) {
-            keep = keep && !(st.bra == y && m > k) &&
-                   (a.tau <= 0.0 || __ldg(a.Qp + bpx[m]) * __ldg(a.Qp + py) >= a.tau);
-          }
+          if constexpr (FAM) keep = keep && !(st.bra == y && m > k) && (a.tau <= 0.0 || s_bq[m] * km.q[k] >= a.tau);
           constexpr bool AGG = (OPT & kStripAgg) != 0;
           if constexpr (AGG) {  // the whole warp digests (shuffle groups), non-kept lanes add zeros
             if (!__any_sync(0xffffffffu, keep)) continue;
           } else {
             if (!keep) continue;
           }
-          PairMeta km;
-          ld_meta_late(a.pm + py, km);
+          const int kbfa = km.bfa[k], kbfb = km.bfb[k];
           const double* v = acc_v[m][k];
           const double deg =
-              (bm.sha != bm.shb ? 2.0 : 1.0) * (km.sha != km.shb ? 2.0 : 1.0) * (bpx[m] != py ? 2.0 : 1.0);
+              (bm.sha != bm.shb ? 2.0 : 1.0) * (km.offd[k] ? 2.0 : 1.0) * (bpx[m] != py ? 2.0 : 1.0);
           const double wj = keep ? 0.5 * deg : 0.0, wk = keep ? 0.25 * deg : 0.0;
-          const int colC = __ldg(a.cpos + km.sha);
-          const int colD = __ldg(a.cpos + km.shb) + (LDOFF ? a.ncolC : 0);
+          const int colC = km.colc[k];
+          const int colD = km.cold[k] + (LDOFF ? a.ncolC : 0);
           const double* Dab = a.D + bm.bfa * n + bm.bfb;
-          const double* Dcd = a.D + km.bfa * n + km.bfb;
+          const double* Dcd = a.D + kbfa * n + kbfb;
           auto dsm = [&](int row, int col, size_t grow, size_t gcol) -> double {
             if constexpr (DSM) return sD[row * ncol + col];
             else return __ldg(a.D + grow * n + gcol);
@@ -289,7 +342,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
                 for (int ib = 0; ib < C::NB; ++ib)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), t);
-              if (keep) red_add(a.J + (km.bfa + ic) * n + km.bfb + id, t * wj, 0);
+              if (keep) red_add(a.J + (kbfa + ic) * n + kbfb + id, t * wj, 0);
             }
           // K_ac += sum_bd v D_bd ; K_ad += sum_bc v D_bc   (rows a of the bra)
           // K_bd += sum_ac v D_ac ; K_bc += sum_ad v D_ad   (rows b of the bra)
@@ -307,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
                 for (int id = 0; id < C::ND; ++id)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rB + ib, colD + id, bm.bfb + ib, km.bfb + id), t);
+                          dsm(rB + ib, colD + id, bm.bfb + ib, kbfb + id), t);
               kidx[ne] = (rA + ia) * ncol + colC + ic;
               kval[ne++] = t * wk;
             }
@@ -319,7 +372,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
                 for (int ic = 0; ic < C::NC; ++ic)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rB + ib, colC + ic, bm.bfb + ib, km.bfa + ic), t);
+                          dsm(rB + ib, colC + ic, bm.bfb + ib, kbfa + ic), t);
               kidx[ne] = (rA + ia) * ncol + colD + id;
               kval[ne++] = t * wk;
             }
@@ -334,7 +387,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
                 for (int ic = 0; ic < C::NC; ++ic)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rA + ia, colC + ic, bm.bfa + ia, km.bfa + ic), t);
+                          dsm(rA + ia, colC + ic, bm.bfa + ia, kbfa + ic), t);
               kidx[ne] = (rB + ib) * ncol + colD + id;
               kval[ne++] = t * wk;
             }
@@ -346,7 +399,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 #pragma unroll
                 for (int id = 0; id < C::ND; ++id)
                   t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rA + ia, colD + id, bm.bfa + ia, km.bfb + id), t);
+                          dsm(rA + ia, colD + id, bm.bfa + ia, kbfb + id), t);
               kidx[ne] = (rB + ib) * ncol + colC + ic;
               kval[ne++] = t * wk;
             }
@@ -389,7 +442,26 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
             reduce_peers<NCK>(pc, cv, lane);
             reduce_peers<NDK>(pd, dv, lane);
             if (keep && __ffs(pc) - 1 == lane) smem_add_batch<NCK>(sK, ci, cv);
-            if (keep && __ffs(pd) - 1 == lane) smem_add_batch<NDK>(sK, di, dv);
+            if (keep && __ffs(pd) - 1 == lane) {
+              if constexpr (OPT & kStripSplitK) {
+                // d-column updates straight to global K (L2 RED.ADD.F64): the
+                // shared-memory atomic unit (~2 cycles per lane) and the L2
+                // atomic units then each carry half of the K traffic
+                int e = 0;
+#pragma unroll
+                for (int ia = 0; ia < C::NA; ++ia)
+#pragma unroll
+                  for (int id = 0; id < C::ND; ++id)
+                    red_add(a.K + (bm.bfa + ia) * n + kbfb + id, dv[e++], 0);
+#pragma unroll
+                for (int ib = 0; ib < C::NB; ++ib)
+#pragma unroll
+                  for (int id = 0; id < C::ND; ++id)
+                    red_add(a.K + (bm.bfb + ib) * n + kbfb + id, dv[e++], 0);
+              } else {
+                smem_add_batch<NDK>(sK, di, dv);
+              }
+            }
           } else if constexpr (OPT & kStripCasBatch) {
             smem_add_batch<NKE>(sK, kidx, kval);
           } else {

@@ -11,13 +11,15 @@ import subprocess
 ap = argparse.ArgumentParser()
 ap.add_argument("rep")
 ap.add_argument("--top", type=int, default=40)
-ap.add_argument("--kernel", default=None, help="ncu -k filter")
+ap.add_argument("--kernel", default=None, help="substring of the kernel name (first match)")
 a = ap.parse_args()
 cmd = ["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass"]
-if a.kernel:
-    cmd += ["-k", a.kernel]
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+sel = next(k for k in range(len(starts) - 1) if a.kernel is None or a.kernel in rows[starts[k]][1])
+print(rows[starts[sel]][1][:150])
+rows = rows[starts[sel]:starts[sel + 1]]
 i0 = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 hdr = rows[i0]
 body = [r for r in rows[i0 + 1:] if len(r) == len(hdr)]
