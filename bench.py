@@ -255,16 +255,24 @@ def run_ours(args, rank, nranks, local_rank):
     # the first SCF iterations). Rank 0 tunes on the whole
     # lists and broadcasts its table: the LPT deal is a function of the
     # lists and the table, so all ranks must share it (disjoint cover).
+    # Then Alg. 2 (combine / measure / revert of the work items per warp
+    # task) on the chosen variants; g is broadcast too.
     t1 = time.perf_counter()
-    table = None
+    table, gran, accepted = None, None, 0
     if rank == 0:
         eng.tune(Dh, reps=2)
         table = eng.get_variants().tolist()
+        accepted = eng.tune_granularity(Dh, reps=3)
+        gran = eng.granularity()
     if dist is not None:
-        obj = [table]
+        obj = [table, gran]
         dist.broadcast_object_list(obj, src=0)
-        table = obj[0]
+        table, gran = obj
     eng.set_variants(table)
+    from paper_2412_13203_b200.eritile import class_table
+    tab = ["".join(map(str, r[:4])) for r in class_table()]
+    for k, g in gran.items():
+        eng.set_granularity(tab.index(k), g)
     tune_s = time.perf_counter() - t1
     chosen = eng.variants()
     tune_table = eng.tune_times() if rank == 0 else {}
@@ -420,6 +428,8 @@ def run_ours(args, rank, nranks, local_rank):
         "clocks": clk.summary(),
         "setup_s": setup_s,
         "tune_s": tune_s,
+        "granularity": {"rule": "Alg. 2: work items per warp task, doubled while the class time drops",
+                        "accepted_combines": accepted, "g": {k: v for k, v in gran.items() if v > 1}},
         "tune_ms": tune_table,
         "classes": [{"cls": "".join(map(str, r["cls"])), "ms": round(r["ms"], 4),
                      "variant": chosen.get(tuple(r["cls"])),

@@ -173,6 +173,35 @@ int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps);
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms);
 /* Variant slots per class (the stride of eritile_gpu_tune_times). */
 int eritile_gpu_max_variants(void);
+
+/* Workload Allocator, Algorithm 2 (SPEC.md:366-425
+ * `tune` / `combine` / `revert` / `measure`): per class, the granularity g
+ * = work items (32 contracted quartets each) fused into one warp task is
+ * doubled (Combine) and kept only if the class's measured time drops
+ * (median of `reps` launches on the class's full work list, warm-up
+ * discarded), else reverted; sweeps repeat while any class improved.
+ * Cap = min(task count, 4096); the coop table kernels are not tunable
+ * (cap 1). Results change only by atomic summation order.
+ *   tune_granularity: the loop to convergence (at most max_sweeps sweeps);
+ *                     returns the number of accepted combines so far.
+ *   tune_step:        one sweep (SCF drivers interleave it with their first
+ *                     iterations); returns 1 if a class
+ *                     improved, 0 once converged.
+ *   get_granularity:  g per class into g[0..cap); returns the class count.
+ *   set_granularity:  g must be a power of two in [1, 4096].
+ *   granularity_history: every measured (g, median ms, spread, accepted)
+ *                     of class cls_index; returns the count.
+ * eritile_alloc_simulate runs the same loop against a mock cost table
+ * (cost[c * stride + k] = time at g = 2^k; no device needed) and returns
+ * the number of accepted combines. */
+int eritile_gpu_tune_granularity(eritile_gpu* ctx, const double* D, int reps, int max_sweeps);
+int eritile_gpu_tune_step(eritile_gpu* ctx, const double* D, int reps);
+int eritile_gpu_get_granularity(const eritile_gpu* ctx, int* g, int cap);
+int eritile_gpu_set_granularity(eritile_gpu* ctx, int cls_index, int g);
+int eritile_gpu_granularity_history(const eritile_gpu* ctx, int cls_index, int cap, int* g, double* ms,
+                                    double* spread, int* accepted);
+int eritile_alloc_simulate(int ncls, const int* cap, const double* cost, int stride, int max_sweeps, int* g_out,
+                           int* sweeps_out);
 int eritile_gpu_set_variant(eritile_gpu* ctx, int cls_index, int var);
 /* The whole variant table (one entry per class, eritile_gpu_num_classes):
  * get returns the class count; set validates every entry first. */

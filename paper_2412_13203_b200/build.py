@@ -73,7 +73,7 @@ def build(jobs: int | None = None, verbose: bool = True) -> Path:
     generate()
     kern_deps = [CSRC / "jk_kernels.cuh", CSRC / "jk_coop.cuh", CSRC / "jk_family.cuh", CSRC / "jk_strip.cuh",
                  CSRC / "jk_api.h"]
-    host_deps = [CSRC / "host" / "molecule.h", CSRC / "host" / "onee.h", CSRC / "jk_api.h",
+    host_deps = [CSRC / "host" / "molecule.h", CSRC / "host" / "onee.h", CSRC / "host" / "allocator.h", CSRC / "jk_api.h",
                  INCLUDE / "eritile_gpu.h"]
     units = []
     # biggest classes first so the long compiles start early

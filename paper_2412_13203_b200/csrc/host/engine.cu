@@ -28,6 +28,7 @@
 #include <thread>
 #include <vector>
 
+#include "allocator.h"
 #include "../../../include/eritile_gpu.h"
 #include "../jk_api.h"
 #include "../jk_kernels.cuh"
@@ -332,7 +333,10 @@ struct eritile_gpu {
   }
 
   // Workload Allocator state: kernel variant per class (kClassTable[c].var)
+  // and the Alg. 2 granularity per class (allocator.h)
   std::vector<int> var_choice;
+  AllocState alloc;
+  int gran(int c) const { return alloc.g.empty() ? 1 : alloc.g[c]; }
   std::vector<double> tune_ms;  // per class launch x kMaxVariants: median ms (tune)
 
   bool profiling = false;
@@ -418,6 +422,75 @@ struct eritile_gpu {
     cudaEventDestroy(e1);
   }
 
+  // Work list of class c under its current variant (-1: no work).
+  int chosen_work(int c) const {
+    for (size_t w = 0; w < work.size(); ++w)
+      if (work[w].cls == c && work[w].fam == uses_fam(c)) return static_cast<int>(w);
+    return -1;
+  }
+  // Alg. 2 caps: min(task count, 4096) for classes whose variant takes the
+  // granularity (lane, unit and strip kernels; the coop table kernels do not).
+  void alloc_caps() {
+    if (alloc.g.empty()) alloc.init(kNumClasses);
+    for (int c = 0; c < kNumClasses; ++c) {
+      const int w = chosen_work(c);
+      const std::string vn = kClassTable[c].var_name[variant(c)];
+      if (w < 0 || vn.rfind("coop", 0) == 0) {
+        alloc.cap[c] = 1;
+        alloc.g[c] = 1;
+        continue;
+      }
+      alloc.cap[c] = static_cast<int>(std::min<long long>(work[w].an, 4096));
+      if (alloc.g[c] > alloc.cap[c]) alloc.g[c] = 1;
+    }
+  }
+  // measure(c, g): median (and spread) of R timed launches of class c's
+  // chosen variant at granularity g on the full work list, warm-up discarded.
+  AllocMeasure measure_class(int c, int g, const double* dDs, double* scratch, int reps, cudaEvent_t e0,
+                             cudaEvent_t e1) {
+    const int w = chosen_work(c);
+    std::vector<double> t;
+    for (int r = 0; r < reps + 1; ++r) {
+      LaunchArgs a = class_args(work[w], dDs, scratch, stream, true);
+      a.gran = g;
+      CK(cudaEventRecord(e0, stream));
+      kClassTable[c].var[variant(c)](a);
+      check_launch(work[w]);
+      CK(cudaEventRecord(e1, stream));
+      CK(cudaEventSynchronize(e1));
+      if (r > 0) t.push_back(elapsed(e0, e1));
+    }
+    std::sort(t.begin(), t.end());
+    return AllocMeasure{t[t.size() / 2], t.back() - t.front()};
+  }
+  // Alg. 2 on the live density: one sweep (SCF interleave) or to convergence.
+  // Returns true if the (last) sweep improved some class.
+  bool tune_granularity(const double* dDs, int reps, int max_sweeps) {
+    alloc_caps();
+    const size_t NN = static_cast<size_t>(nbf) * nbf;
+    DevBuf<double> scratch;
+    scratch.alloc(2 * NN);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    bool improved = false;
+    try {
+      auto m = [&](int c, int g) { return measure_class(c, g, dDs, scratch.p, reps, e0, e1); };
+      const int s0 = alloc.sweeps;
+      while (alloc.sweeps - s0 < max_sweeps) {
+        improved = alloc_sweep(alloc, m);
+        if (!improved) break;
+      }
+    } catch (...) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return improved;
+  }
+
   // full = true: the class's whole (unsharded) list (the allocator times
   // those); else this rank's share.
   LaunchArgs class_args(const ClassWork& cw, const double* dDs, double* dJK, cudaStream_t st,
@@ -452,6 +525,7 @@ struct eritile_gpu {
       a.cpos = d_cpos.p;
     }
     a.kmeta = cw.fam ? d_kmu.p : d_kmp.p;
+    a.gran = gran(cw.cls);
     if (cw.fam) {
       a.um = d_um.p;
       a.uw = d_uw.p;
@@ -1983,6 +2057,87 @@ int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps) {
 }
 
 int eritile_gpu_max_variants(void) { return kMaxVariants; }
+
+static int tune_gran_entry(eritile_gpu* ctx, const double* D, int reps, int max_sweeps, int* improved) {
+  return guard(ctx, [&] {
+    ctx->check_ready();
+    ctx->ensure_mats();
+    const size_t NN = static_cast<size_t>(ctx->nbf) * ctx->nbf;
+    ctx->d_D.alloc(NN);
+    CK(cudaMemcpyAsync(ctx->d_D.p, D, sizeof(double) * NN, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->prescale(ctx->d_D.p, ctx->d_Ds.p, ctx->stream);
+    *improved = ctx->tune_granularity(ctx->d_Ds.p, reps, max_sweeps) ? 1 : 0;
+  });
+}
+
+int eritile_gpu_tune_granularity(eritile_gpu* ctx, const double* D, int reps, int max_sweeps) {
+  if (!ctx || !D || reps < 1 || max_sweeps < 1) return ERITILE_ERR_ARG;
+  int improved = 0;
+  const int rc = tune_gran_entry(ctx, D, reps, max_sweeps, &improved);
+  return rc != 0 ? rc : ctx->alloc.accepted;
+}
+
+int eritile_gpu_tune_step(eritile_gpu* ctx, const double* D, int reps) {
+  if (!ctx || !D || reps < 1) return ERITILE_ERR_ARG;
+  int improved = 0;
+  const int rc = tune_gran_entry(ctx, D, reps, 1, &improved);
+  return rc != 0 ? rc : improved;
+}
+
+int eritile_gpu_get_granularity(const eritile_gpu* ctx, int* g, int cap) {
+  if (!ctx) return ERITILE_ERR_ARG;
+  if (g)
+    for (int c = 0; c < std::min(cap, kNumClasses); ++c) g[c] = ctx->gran(c);
+  return kNumClasses;
+}
+
+int eritile_gpu_set_granularity(eritile_gpu* ctx, int cls_index, int g) {
+  if (!ctx || cls_index < 0 || cls_index >= kNumClasses || g < 1 || g > 4096 || (g & (g - 1)) != 0)
+    return ERITILE_ERR_ARG;
+  if (ctx->alloc.g.empty()) ctx->alloc.init(kNumClasses);
+  ctx->alloc.g[cls_index] = g;
+  return 0;
+}
+
+int eritile_gpu_granularity_history(const eritile_gpu* ctx, int cls_index, int cap, int* g, double* ms,
+                                    double* spread, int* accepted) {
+  if (!ctx || cls_index < 0 || cls_index >= kNumClasses) return ERITILE_ERR_ARG;
+  if (ctx->alloc.history.empty()) return 0;
+  const auto& h = ctx->alloc.history[cls_index];
+  for (int k = 0; k < std::min<int>(cap, static_cast<int>(h.size())); ++k) {
+    if (g) g[k] = h[k].g;
+    if (ms) ms[k] = h[k].median;
+    if (spread) spread[k] = h[k].spread;
+    if (accepted) accepted[k] = h[k].accepted ? 1 : 0;
+  }
+  return static_cast<int>(h.size());
+}
+
+int eritile_alloc_simulate(int ncls, const int* cap, const double* cost, int stride, int max_sweeps, int* g_out,
+                           int* sweeps_out) {
+  if (ncls < 1 || !cap || !cost || stride < 1 || max_sweeps < 1 || !g_out) return ERITILE_ERR_ARG;
+  AllocState s;
+  s.init(ncls);
+  for (int c = 0; c < ncls; ++c) {
+    s.cap[c] = cap[c];
+    long long need = 1;
+    int k = 0;
+    while (need * 2 <= cap[c]) {
+      need *= 2;
+      ++k;
+    }
+    if (k >= stride) return ERITILE_ERR_ARG;  // the table must cover g = 1 .. cap
+  }
+  auto m = [&](int c, int g) {
+    int k = 0;
+    while ((1 << k) < g) ++k;
+    return AllocMeasure{cost[static_cast<size_t>(c) * stride + k], 0.0};
+  };
+  alloc_tune(s, m, max_sweeps);
+  for (int c = 0; c < ncls; ++c) g_out[c] = s.g[c];
+  if (sweeps_out) *sweeps_out = s.sweeps;
+  return s.accepted;
+}
 
 int eritile_gpu_tune_times(const eritile_gpu* ctx, int cap, int* cls_index, double* ms) {
   if (!ctx) return ERITILE_ERR_ARG;

@@ -101,6 +101,7 @@ struct LaunchArgs {
   int N;
   const double* boys_tab;  // kBoysMmax+1 slices of kBoysRows*kBoysCols
   cudaStream_t stream;
+  int gran;   // Workload Allocator granularity: consecutive work items per warp task (>= 1)
   int grid;   // 0 = auto
   int block;  // threads per CTA
   // family (unit) launches: work items index units

@@ -162,9 +162,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
   (void)staged;
   const size_t n = static_cast<size_t>(a.N);
   const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  for (long long w = i0 + static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < i1;
-       w += warps) {
-    const WorkItem it = a.items[w];
+  auto process = [&](const WorkItem& it) {
     const int nq = it.r0nq >> 24;
     const bool active = lane < nq;
     int q = (it.r0nq & 0xffffff) + (active ? lane : 0);
@@ -314,7 +312,9 @@ __global__ void __launch_bounds__(NT, MINB) jk_fam_kernel(LaunchArgs a, long lon
           if (tail && s != 0.0) red_add(a.J + (bm.bfa + ia) * n + bm.bfb + ib, s, a.det);
         }
     }
-  }
+  };
+  for_warp_items(a.items, i0, i1, a.gran, static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5),
+                 warps, process);
 }
 
 template <class C, int MB, int MK, int MINB, int STYLE, int NT>
@@ -325,7 +325,8 @@ void launch_fam_seg(const LaunchArgs& a, long long i0, long long i1) {
   const LaunchSetup ls =
       launch_setup(reinterpret_cast<const void*>(jk_fam_kernel<C, MB, MK, MINB, STYLE, NT>), NT, smem, true);
   if (!ls.bps) return;  // CUDA error pending for the caller's check
-  const long long want = (i1 - i0 + (NT / 32) - 1) / (NT / 32);
+  const long long g = a.gran > 1 ? a.gran : 1;
+  const long long want = ((i1 - i0 + g - 1) / g + (NT / 32) - 1) / (NT / 32);
   const long long cap = static_cast<long long>(ls.bps) * ls.sms;
   const int grid = static_cast<int>(want < cap ? want : cap);
   jk_fam_kernel<C, MB, MK, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a, i0, i1);

@@ -369,6 +369,29 @@ __device__ __forceinline__ void load_boys_slice(double* s_boys, const double* bo
 
 constexpr int kJkThreads = 256;
 
+// Work items [i0, i1) in warp tasks of `gran` consecutive items (the
+// Workload Allocator's Combine granularity), tasks dealt
+// round-robin over the grid's warps; f(item) per item in order. The next
+// item's descriptor is fetched one item ahead (hides its L2 trip).
+template <class F>
+__device__ __forceinline__ void for_warp_items(const WorkItem* __restrict__ items, long long i0, long long i1,
+                                               int gran, long long wid, long long warps, F&& f) {
+  const long long g = gran > 1 ? gran : 1;
+  const long long ntask = (i1 - i0 + g - 1) / g;
+  long long t = wid, w = i0 + t * g, e = w + g < i1 ? w + g : i1;
+  WorkItem nxt = t < ntask ? items[w] : WorkItem{};
+  while (t < ntask) {
+    const WorkItem it = nxt;
+    if (++w >= e) {
+      t += warps;
+      w = i0 + t * g;
+      e = w + g < i1 ? w + g : i1;
+    }
+    if (t < ntask) nxt = items[w];
+    f(it);
+  }
+}
+
 // Shared-memory carveout just large enough for the resident CTAs, so the
 // rest of the SM's 256 KB L1/shared array caches primitive records.
 inline cudaError_t set_min_carveout(const void* fn, int blocks_per_sm, size_t smem) {
@@ -391,6 +414,11 @@ struct LaunchSetup {
 inline LaunchSetup launch_setup(const void* fn, int nt, size_t smem, bool min_carveout) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, size_t>, LaunchSetup> cache;
+  // the dynamic shared-memory opt-in is one attribute per (kernel, device):
+  // it only ever grows, so a launch with a smaller size after a larger one
+  // (another molecule, another class column count) never lowers it below a
+  // size whose setup is already cached
+  static std::map<std::pair<const void*, int>, size_t> attr;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return {0, 0};
   std::lock_guard<std::mutex> lk(mu);
@@ -398,12 +426,17 @@ inline LaunchSetup launch_setup(const void* fn, int nt, size_t smem, bool min_ca
   const auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   LaunchSetup s{0, 0};
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.bps, fn, nt, smem) != cudaSuccess ||
+  size_t& cur = attr[std::make_pair(fn, dev)];
+  if (smem > cur) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+      return {0, 0};
+    cur = smem;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.bps, fn, nt, smem) != cudaSuccess ||
       cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return {0, 0};
   if (s.bps < 1) s.bps = 1;
-  if (min_carveout && set_min_carveout(fn, s.bps, smem) != cudaSuccess) return {0, 0};
+  if (min_carveout && set_min_carveout(fn, s.bps, cur) != cudaSuccess) return {0, 0};
   cache.emplace(key, s);
   return s;
 }
@@ -416,7 +449,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
                                                        const double* __restrict__ D, double* __restrict__ J,
                                                        double* __restrict__ K, int N,
                                                        const double* __restrict__ boys_tab,
-                                                       const PrimRec* __restrict__ kprims, int det) {
+                                                       const PrimRec* __restrict__ kprims, int det, int gran) {
   extern __shared__ __align__(16) double s_boys[];
   load_boys_for<C>(s_boys, boys_tab);
 
@@ -581,14 +614,8 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
         }
     }
   };
-  long long w = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  WorkItem nxt = w < nitems ? items[w] : WorkItem{};
-  for (; w < nitems; w += warps) {
-    // the next task's descriptor is fetched one task ahead (hides its L2 trip)
-    const WorkItem it = nxt;
-    if (w + warps < nitems) nxt = items[w + warps];
-    process(it);
-  }
+  for_warp_items(items, 0, nitems, gran, static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5),
+                 warps, process);
 }
 
 // Schwarz diagonal: Q_x = sqrt(max_{mu,nu} |(mu nu|mu nu)|) over normalised
@@ -655,11 +682,12 @@ void launch_class(const LaunchArgs& a) {
     const LaunchSetup ls =
         launch_setup(reinterpret_cast<const void*>(jk_kernel<C, MINB, STYLE, NT>), NT, smem, true);
     if (!ls.bps) return;  // CUDA error pending for the caller's check
-    const long long want = (a.nitems + (NT / 32) - 1) / (NT / 32);
+    const long long g = a.gran > 1 ? a.gran : 1;
+    const long long want = ((a.nitems + g - 1) / g + (NT / 32) - 1) / (NT / 32);
     const long long cap = static_cast<long long>(ls.bps) * ls.sms;
     const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
     jk_kernel<C, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
-                                                       a.K, a.N, a.boys_tab, a.kprims, a.det);
+                                                       a.K, a.N, a.boys_tab, a.kprims, a.det, a.gran);
   } else if (a.mode == 2) {
     if (a.nq <= 0) return;
     cudaFuncSetAttribute(quartet_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -51,17 +51,19 @@ __device__ __forceinline__ void smem_add_batch(double* sK, const int (&idx)[NE],
   unsigned long long old[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) old[e] = *reinterpret_cast<volatile unsigned long long*>(sK + idx[e]);
-  unsigned pend = 0;
+  bool lost[NE];  // (static indices: predicates, any NE)
+  bool any = false;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const unsigned long long nw = __double_as_longlong(__longlong_as_double(old[e]) + val[e]);
     const unsigned long long r = atomicCAS(reinterpret_cast<unsigned long long*>(sK + idx[e]), old[e], nw);
-    if (r != old[e]) pend |= 1u << e;
+    lost[e] = r != old[e];
+    any = any || lost[e];
   }
-  if (pend) {  // (static indices: the arrays stay in registers)
+  if (any) {
 #pragma unroll
     for (int e = 0; e < NE; ++e)
-      if (pend >> e & 1u) atomicAdd(sK + idx[e], val[e]);
+      if (lost[e]) atomicAdd(sK + idx[e], val[e]);
   }
 }
 
@@ -195,11 +197,22 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       bpx[0] = st.bra;
     }
     (void)warp;
-    int wn = 0;
+    // items are claimed in runs of g = a.gran consecutive items (the
+    // Workload Allocator's Combine granularity); s_next may overshoot i1
+    const int g = a.gran > 1 ? a.gran : 1;
+    int lo = 0, hi = 0;  // this warp's claimed, not yet started items
+    auto claim = [&]() -> bool {
+      int c = 0;
+      if (lane == 0) c = atomicAdd(&s_next, g);  // dynamic: items differ in primitive count
+      c = __shfl_sync(0xffffffffu, c, 0);
+      lo = c;
+      hi = c + g < st.i1 ? c + g : st.i1;
+      return c < st.i1;
+    };
+    int wn = st.i1;
     WorkItem nxt{};
     if constexpr (OPT & kStripItemPf) {
-      if (lane == 0) wn = atomicAdd(&s_next, 1);
-      wn = __shfl_sync(0xffffffffu, wn, 0);
+      if (claim()) wn = lo++;
       if (wn < st.i1) nxt = a.items[wn];
     }
     for (;;) {
@@ -209,16 +222,15 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         w = wn;
         if (w >= st.i1) break;
         it = nxt;
-        if (lane == 0) wn = atomicAdd(&s_next, 1);
-        wn = __shfl_sync(0xffffffffu, wn, 0);
+        wn = st.i1;
+        if (lo < hi || claim()) wn = lo++;
         if (wn < st.i1) nxt = a.items[wn];  // in flight during this item
-
       } else {
-        if (lane == 0) w = atomicAdd(&s_next, 1);  // dynamic: items differ in primitive count
-        w = __shfl_sync(0xffffffffu, w, 0);
-        if (w >= st.i1) break;
+        if (lo >= hi && !claim()) break;
+        w = lo++;
         it = a.items[w];
       }
+      (void)w;
       const int nq = it.r0nq >> 24;
       const bool active = lane < nq;
       const int y = it.yfirst + (it.r0nq & 0xffffff) + (active ? lane : 0);  // single-bra item

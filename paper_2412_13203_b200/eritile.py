@@ -92,6 +92,14 @@ def _lib():
         "eritile_gpu_set_variant": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
         "eritile_gpu_tune_times": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
         "eritile_gpu_max_variants": (C.c_int, []),
+        "eritile_gpu_tune_granularity": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+        "eritile_gpu_tune_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+        "eritile_gpu_get_granularity": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+        "eritile_gpu_set_granularity": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+        "eritile_gpu_granularity_history": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                                      C.c_void_p, C.c_void_p]),
+        "eritile_alloc_simulate": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                             C.c_void_p]),
         "eritile_gpu_set_families": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_set_concurrent": (C.c_int, [C.c_void_p, C.c_int]),
         "eritile_gpu_set_strips": (C.c_int, [C.c_void_p, C.c_longlong, C.c_int]),
@@ -376,6 +384,50 @@ class Engine:
         self._check(self._lib.eritile_gpu_set_variant(self._h, int(cls_index), int(var)))
         return self
 
+    def tune_granularity(self, D: np.ndarray, reps: int = 3, max_sweeps: int = 64) -> int:
+        """Workload Allocator Alg. 2: per
+        class, double the work items per warp task while the measured class
+        time drops (combine / measure / revert), to convergence. Returns the
+        number of accepted combines."""
+        D = np.ascontiguousarray(D, dtype=np.float64)
+        rc = self._lib.eritile_gpu_tune_granularity(self._h, D.ctypes.data, reps, max_sweeps)
+        if rc < 0:
+            self._check(rc)
+        return rc
+
+    def tune_step(self, D: np.ndarray, reps: int = 3) -> bool:
+        """One Alg. 2 sweep over the classes (SCF drivers interleave it with
+        their first iterations). True if some class improved."""
+        D = np.ascontiguousarray(D, dtype=np.float64)
+        rc = self._lib.eritile_gpu_tune_step(self._h, D.ctypes.data, reps)
+        if rc < 0:
+            self._check(rc)
+        return rc == 1
+
+    def granularity(self) -> dict:
+        """{class (la,lb,lc,ld) string: g} for every class."""
+        n = self._lib.eritile_gpu_get_granularity(self._h, None, 0)
+        g = np.zeros(n, np.int32)
+        self._lib.eritile_gpu_get_granularity(self._h, g.ctypes.data, n)
+        tab = class_table()
+        return {"".join(map(str, tab[c][:4])): int(g[c]) for c in range(n)}
+
+    def set_granularity(self, cls_index: int, g: int) -> "Engine":
+        self._check(self._lib.eritile_gpu_set_granularity(self._h, cls_index, g))
+        return self
+
+    def granularity_history(self, cls_index: int):
+        """[(g, median ms, spread ms, accepted)] of every Alg. 2 measurement."""
+        n = self._lib.eritile_gpu_granularity_history(self._h, cls_index, 0, None, None, None, None)
+        if n < 0:
+            self._check(n)
+        g = np.zeros(max(n, 1), np.int32)
+        ms, sp = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        acc = np.zeros(max(n, 1), np.int32)
+        self._lib.eritile_gpu_granularity_history(self._h, cls_index, n, g.ctypes.data, ms.ctypes.data,
+                                                  sp.ctypes.data, acc.ctypes.data)
+        return [(int(g[k]), float(ms[k]), float(sp[k]), bool(acc[k])) for k in range(n)]
+
     def tune_times(self) -> dict:
         """{class: {variant name: median ms}} of the last tune."""
         n = self._lib.eritile_gpu_tune_times(self._h, 0, None, None)
@@ -402,6 +454,22 @@ class Engine:
         s = Stats()
         self._check(self._lib.eritile_gpu_get_stats(self._h, C.byref(s)))
         return s.as_dict()
+
+
+def alloc_simulate(cost, cap, max_sweeps: int = 64):
+    """Run the Workload Allocator loop (Alg. 2, csrc/host/allocator.h) against
+    a mock cost table: cost[c][k] = time of class c at g = 2**k (no device).
+    Returns (g per class, accepted combines, sweeps)."""
+    cost = np.ascontiguousarray(cost, dtype=np.float64)
+    cap = np.ascontiguousarray(cap, dtype=np.int32)
+    ncls, stride = cost.shape
+    g = np.zeros(ncls, np.int32)
+    sweeps = np.zeros(1, np.int32)
+    acc = _lib().eritile_alloc_simulate(ncls, cap.ctypes.data, cost.ctypes.data, stride, max_sweeps, g.ctypes.data,
+                                        sweeps.ctypes.data)
+    if acc < 0:
+        raise ValueError("alloc_simulate: bad arguments (the cost table must cover g = 1 .. cap)")
+    return g, int(acc), int(sweeps[0])
 
 
 def variant_names(cls_index: int):

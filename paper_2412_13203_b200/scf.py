@@ -23,6 +23,7 @@ class ScfResult:
     energies: List[float] = field(default_factory=list)
     density: Optional[np.ndarray] = None
     fock_builds: int = 0
+    tune_sweeps: int = 0  # Workload Allocator sweeps interleaved with the first iterations
 
 
 def orthogonalizer(S: np.ndarray, tol: float = 1e-10) -> np.ndarray:
@@ -180,10 +181,34 @@ def _rhf_device(engine, S, H, e_nuc, nocc, conv, max_iter, diis, e_conv, st) -> 
     return res
 
 
+def interleave_tuning(engine, build_jk: Callable[[np.ndarray], tuple], tune_variants: bool = True,
+                      reps: int = 3):
+    """Wrap a Fock build so the Workload Allocator runs inside the first SCF
+    iterations on the live density ("integrates with ongoing
+    computations at runtime"): the first build picks the kernel
+    variant per class, then every build runs one Alg. 2 sweep (combine /
+    measure / revert of the granularity) until a sweep finds no improvement.
+    Tuning changes J/K only by atomic summation order. Returns (build, state)."""
+    state = {"sweeps": 0, "converged": False, "variants": not tune_variants}
+
+    def build(D):
+        if not state["variants"]:
+            engine.tune(D, reps=reps)
+            state["variants"] = True
+        if not state["converged"]:
+            state["converged"] = not engine.tune_step(D, reps)
+            state["sweeps"] += 1
+        return build_jk(D)
+
+    return build, state
+
+
 def run_rhf(xyz_text: str, basis_text: str, tau: float = 1e-12, device: int = 0, kappa_screen: float = 0.0,
-            device_resident: bool = False, **kw) -> ScfResult:
+            device_resident: bool = False, tune: bool = False, **kw) -> ScfResult:
     """Full driver on one GPU: load, pairs, Schwarz, screening, SCF. With
-    ``device_resident`` the post-Fock step runs on the GPU too (rhf_device)."""
+    ``device_resident`` the post-Fock step runs on the GPU too (rhf_device).
+    With ``tune`` the Workload Allocator is interleaved with the first
+    iterations (interleave_tuning)."""
     from .eritile import Engine
     e = Engine(device).load_molecule(xyz_text, basis_text).build_pairs(kappa_screen)
     e.set_screening(tau)
@@ -192,4 +217,11 @@ def run_rhf(xyz_text: str, basis_text: str, tau: float = 1e-12, device: int = 0,
         import torch
         torch.cuda.set_device(device)
         return rhf_device(e, S, T + V, e.nuclear_repulsion(), e.nelectrons // 2, **kw)
-    return rhf(e.build_jk, S, T + V, e.nuclear_repulsion(), e.nelectrons // 2, **kw)
+    build = e.build_jk
+    state = None
+    if tune:
+        build, state = interleave_tuning(e, e.build_jk)
+    res = rhf(build, S, T + V, e.nuclear_repulsion(), e.nelectrons // 2, **kw)
+    if state is not None:
+        res.tune_sweeps = state["sweeps"]
+    return res

@@ -40,8 +40,8 @@ def test_boys_device_vs_reference(gpu):
 
 
 def test_boys_device_uniform_warps(gpu):
-    """The warp-uniform Boys branches (every lane T < 40, every lane T >= 40)
-    give the same values as the reference (boys.hpp:23-44) as the mixed one."""
+    """Warps whose lanes all sit below T = 40, all above, or straddle it give
+    the reference values (boys.hpp:23-44) from the straight-line Boys form."""
     from paper_2412_13203_b200.eritile import Engine
     e = Engine(0)
     o = Oracle("orc")
@@ -362,22 +362,23 @@ def test_strip_kernels_vs_oracle(gpu, mol, basis, kappa, smin, smax):
     Jo, Ko, nq = O.build_jk(D, tau)
     ox, oy = O.quartets(tau)
     order = np.lexsort((oy, ox))
+    ncls = len(class_table())
     for fam in (False, True):
         e = Engine(0).load_molecule(xyz, bas).build_pairs(kappa)
         e.set_families(fam).set_strips(smin, smax)
         e.set_screening(tau)
-        nstrip = 0
-        for i in range(len(class_table())):
-            names = variant_names(i)
-            want = "fstrip" if fam else "strip"
-            k = next((j for j, n in enumerate(names) if n.startswith(want)), None)
-            if k is not None:
-                e.set_variant(i, k)
-                nstrip += 1
-        assert nstrip > 0
-        J, K = e.build_jk(D)
         xs, ys = e.quartets()
         assert np.array_equal(xs, ox[order]) and np.array_equal(ys, oy[order])
         assert nq == e.num_quartets()
-        assert np.max(np.abs(J - Jo)) < 1e-10 and np.max(np.abs(K - Ko)) < 1e-10, (fam, np.max(np.abs(J - Jo)),
-                                                                                    np.max(np.abs(K - Ko)))
+        # every strip variant (loop styles, batched / aggregated / split K
+        # updates, prefetch options), each on every class that has it
+        want = "fstrip" if fam else "strip"
+        vnames = sorted({n for i in range(ncls) for n in variant_names(i) if n.startswith(want)})
+        assert vnames
+        for vn in vnames:
+            for i in range(ncls):
+                if vn in variant_names(i):
+                    e.set_variant(i, vn)
+            J, K = e.build_jk(D)
+            dj, dk = np.max(np.abs(J - Jo)), np.max(np.abs(K - Ko))
+            assert dj < 1e-10 and dk < 1e-10, (fam, vn, dj, dk)
