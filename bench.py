@@ -40,7 +40,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--waters", type=int, default=80)
     ap.add_argument("--basis", default="cc-pvdz")
-    ap.add_argument("--geom", default="", help="geometry fixture (e.g. benzene) instead of the water cluster")
+    ap.add_argument("--geom", default="", help="geometry fixture (e.g. benzene) or ala<n> (idealised "
+                                                 "H-(Ala)_n-OH strand, config 5) instead of the water cluster")
     ap.add_argument("--tau", type=float, default=1e-10)
     ap.add_argument("--kappa", type=float, default=1e-14,
                     help="reference primitive-pair screen |coef|*kappa < thr (block.hpp:83-89; "
@@ -57,8 +58,11 @@ BASIS_FILES = {"sto-3g": "sto-3g.txt", "6-31g*": "6-31gs.txt", "cc-pvdz": "cc-pv
 
 def workload(args):
     from paper_2412_13203_b200.eritile import read_fixture
-    from paper_2412_13203_b200.geometry import water_cluster
-    xyz = read_fixture("geom", args.geom + ".xyz") if args.geom else water_cluster(args.waters)
+    from paper_2412_13203_b200.geometry import alanine_chain, water_cluster
+    if args.geom.startswith("ala") and args.geom[3:].isdigit():
+        xyz = alanine_chain(int(args.geom[3:]))
+    else:
+        xyz = read_fixture("geom", args.geom + ".xyz") if args.geom else water_cluster(args.waters)
     return xyz, read_fixture("basis", BASIS_FILES[args.basis])
 
 

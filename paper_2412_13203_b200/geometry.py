@@ -95,3 +95,96 @@ def to_xyz(atoms, comment: str = "") -> str:
 
 def water_cluster(n: int, seed: int = 2412) -> str:
     return to_xyz(water_cluster_atoms(n, seed), f"(H2O)_{n} lattice, spacing 3.1 A, mt19937_64({seed})")
+
+
+# ---- (Ala)_n: idealised extended polyalanine ----
+#
+# Taxol coordinates are not available offline, so the config-5 workload (an
+# f-shell, N-containing, peptide-like L mix at cc-pVTZ) is an idealised
+# H-(Ala)_n-OH strand built from standard peptide internal coordinates
+# (Engh & Huber bond lengths / angles; planar trans peptides, omega = 180;
+# extended beta strand phi = -139, psi = +135 degrees by default) with the
+# natural extension reference frame (NeRF). Deterministic, no randomness.
+
+def _sub(a, b):
+    return (a[0] - b[0], a[1] - b[1], a[2] - b[2])
+
+
+def _add(a, b):
+    return (a[0] + b[0], a[1] + b[1], a[2] + b[2])
+
+
+def _scale(a, s):
+    return (a[0] * s, a[1] * s, a[2] * s)
+
+
+def _norm(a):
+    n = math.sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2])
+    return (a[0] / n, a[1] / n, a[2] / n)
+
+
+def _cross(a, b):
+    return (a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0])
+
+
+def _place(a, b, c, bond: float, angle_deg: float, dihedral_deg: float):
+    """NeRF: the atom d bonded to c with |cd| = bond, angle(b, c, d) and
+    dihedral(a, b, c, d) given in degrees."""
+    th, ph = math.radians(angle_deg), math.radians(dihedral_deg)
+    bc = _norm(_sub(c, b))
+    n = _norm(_cross(_sub(b, a), bc))
+    m = _cross(n, bc)
+    d2 = (-bond * math.cos(th), bond * math.sin(th) * math.cos(ph), bond * math.sin(th) * math.sin(ph))
+    return _add(c, _add(_scale(bc, d2[0]), _add(_scale(m, d2[1]), _scale(n, d2[2]))))
+
+
+def alanine_chain_atoms(n: int, phi: float = -139.0, psi: float = 135.0, omega: float = 180.0):
+    if n < 1:
+        raise ValueError("alanine_chain: n >= 1")
+    # backbone N, CA, C of every residue, then one virtual N for the C-terminus
+    bb = [(0.0, 0.0, 0.0), (1.458, 0.0, 0.0)]
+    bb.append(_place((0.0, 1.0, 0.0), bb[0], bb[1], 1.525, 111.2, -60.0))
+    for i in range(1, n + 1):
+        N = _place(bb[-3], bb[-2], bb[-1], 1.329, 116.2, psi)      # C(i-1)-N(i), dihedral N-CA-C-N = psi
+        if i == n:
+            bb.append(N)
+            break
+        CA = _place(bb[-2], bb[-1], N, 1.458, 121.7, omega)        # omega: CA-C-N-CA
+        C = _place(bb[-1], N, CA, 1.525, 111.2, phi)               # phi: C-N-CA-C
+        bb += [N, CA, C]
+    atoms = []
+    for i in range(n):
+        N, CA, C = bb[3 * i], bb[3 * i + 1], bb[3 * i + 2]
+        Nn = bb[3 * i + 3]  # next residue's N (the C-terminal OXT position for the last one)
+        Cp = bb[3 * i - 1] if i > 0 else None
+        atoms.append(("N", N))
+        if Cp is None:  # N-terminal NH2
+            atoms.append(("H", _place(C, CA, N, 1.01, 109.5, 120.0)))
+            atoms.append(("H", _place(C, CA, N, 1.01, 109.5, -120.0)))
+        else:  # amide H in the peptide plane, bisecting the external angle at N
+            u = _norm(_add(_norm(_sub(N, Cp)), _norm(_sub(N, CA))))
+            atoms.append(("H", _add(N, _scale(u, 1.01))))
+        atoms.append(("C", CA))
+        # HA and CB: the two remaining tetrahedral positions at CA (L configuration)
+        bis = _norm(_add(_norm(_sub(CA, N)), _norm(_sub(CA, C))))
+        nrm = _norm(_cross(_sub(N, CA), _sub(C, CA)))
+        h = math.radians(54.75)
+        cb = _add(CA, _scale(_add(_scale(bis, math.cos(h)), _scale(nrm, math.sin(h))), 1.530))
+        ha = _add(CA, _scale(_add(_scale(bis, math.cos(h)), _scale(nrm, -math.sin(h))), 1.090))
+        atoms.append(("H", ha))
+        atoms.append(("C", cb))
+        for dih in (60.0, 180.0, 300.0):
+            atoms.append(("H", _place(N, CA, cb, 1.090, 109.5, dih)))
+        atoms.append(("C", C))
+        u = _norm(_add(_norm(_sub(C, CA)), _norm(_sub(C, Nn))))
+        atoms.append(("O", _add(C, _scale(u, 1.231))))
+        if i == n - 1:  # C-terminal OH at the virtual next-N position
+            oxt = _add(C, _scale(_norm(_sub(Nn, C)), 1.340))
+            atoms.append(("O", oxt))
+            atoms.append(("H", _place(CA, C, oxt, 0.970, 106.0, 180.0)))
+    return atoms
+
+
+def alanine_chain(n: int, **kw) -> str:
+    """H-(Ala)_n-OH extended strand (10 n + 2 atoms), XYZ in Angstrom."""
+    return to_xyz(alanine_chain_atoms(n, **kw), f"H-(Ala)_{n}-OH extended strand (idealised internal coordinates)")
