@@ -177,6 +177,16 @@ def ncu_traffic(workload: str, kernel: str):
 
 
 # ------------------------------------------------------------------ CPU arm
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample(args, steps: int, warmup: int, target_s: float, reference_arm: bool):
     """Reference CPU path on the host cores: oracle/_ref (unmodified reference
     headers + SPEC executor) when present, else the C restatement."""
@@ -211,7 +221,13 @@ def cpu_sample(args, steps: int, warmup: int, target_s: float, reference_arm: bo
             qs += nq
             ts += dt
     value = qs / ts if ts > 0 else rate
-    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+    # one host thread on a smaller sample (~target_s / 4): the per-core rate
+    st1 = max(per_step, int(per_step * cores * 4))
+    st1 = min(st1, nblocks)
+    _, _, nq1, dt1 = S.build_jk_timed(D, args.tau, 1, st1, 0)
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+            "value_1thread": nq1 / max(dt1, 1e-9),
+            "sample_1thread": f"every {st1}-th QuadBlock, {nq1} quartets in {dt1:.1f} s on 1 thread",
             "sample": f"every {per_step}-th of {nblocks} QuadBlocks (M=32) per step, {steps} steps, "
                       f"{qs} quartets in {ts:.1f} s of parallel ERI+digestion time "
                       f"(partial-matrix merge and the {tq:.1f} s Schwarz diagonal excluded)",
@@ -318,13 +334,16 @@ def run_ours(args, rank, nranks, local_rank):
     # time the device API + all-reduce with pinned host copies instead (a
     # single rank's build_jk is a partial sum there).
     if nranks == 1:
-        e2e_api = "eritile_gpu_build_jk (host buffers, pageable numpy)"
+        e2e_api = "eritile_gpu_build_jk (host buffers: page-locked numpy arrays)"
+        Dpin = torch.from_numpy(Dh).pin_memory().numpy()
+        Jpin = torch.empty((N, N), dtype=torch.float64).pin_memory().numpy()
+        Kpin = torch.empty((N, N), dtype=torch.float64).pin_memory().numpy()
         e2e_t = []
         for k in range(max(args.steps, 1)):
             flush.fill_(float(k))
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            Jh, Kh = eng.build_jk(Dh)
+            Jh, Kh = eng.build_jk(Dpin, out=(Jpin, Kpin))
             e2e_t.append(time.perf_counter() - t0)
         e2e_ms = 1e3 * sum(e2e_t) / len(e2e_t)
     else:

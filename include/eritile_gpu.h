@@ -159,14 +159,23 @@ int eritile_gpu_get_stats(const eritile_gpu* ctx, eritile_gpu_stats* out);
 int eritile_gpu_set_profiling(eritile_gpu* ctx, int on);
 int eritile_gpu_class_profile(eritile_gpu* ctx, int cap, int* cls4, double* ms, double* flops,
                               long long* quartets, long long* prim_quartets);
-/* Workload Allocator (Alg. 2; SPEC.md:367-438 tune): time
- * every kernel variant of every class on its whole (unsharded) work list on
+/* Workload Allocator, first stage (kernel variant per class): time every
+ * kernel variant of every class on its whole (unsharded) work list on
  * density D (host, N x N), median of `reps` launches each, and keep the
- * fastest per class. Variant families (eritile_gpu_variant_name):
- * "lane_*" one lane per contracted quartet running the class's straight-line
- * plan (loop style x CTA shape x register budget), "fam_*" the same over
- * shared-primitive units, "coop"/"coopw" the CTA-/warp-cooperative
- * level-scheduled plan. The choice changes atomic summation order only. */
+ * fastest per class. The second stage is Algorithm 2 proper
+ * (eritile_gpu_tune_granularity below). Variant families
+ * (eritile_gpu_variant_name):
+ *   "lane_*"   one lane per contracted quartet running the class's
+ *              straight-line plan (loop style x CTA shape x register budget);
+ *   "fam_*"    the same over shared-primitive units (sibling shells);
+ *   "strip_*" / "fstrip_*"  bra-stationary strips (pair / unit lists): K rows
+ *              of the bra in shared memory, flushed once per strip; suffixes
+ *              _o7 (batched CAS + prefetch), _a (warp-aggregated K updates),
+ *              _k2 (two ket primitives per bra record), _p (L1 prefetch),
+ *              _s (d-column K updates to global memory), _tNNN CTA size;
+ *   "coop" / "coopw"  the CTA- / warp-cooperative level-scheduled plan
+ *              (high L).
+ * The choice changes atomic summation order only. */
 int eritile_gpu_tune(eritile_gpu* ctx, const double* D, int reps);
 /* Per class of the last tune: class table index and the median ms of each
  * variant (eritile_gpu_max_variants() slots per class, 0 = not timed). */

@@ -55,8 +55,6 @@ def ncart(L: int) -> int:
 
 
 DIRS = "xyz"
-# the two-ket loop variant only for the smallest plans (register budget)
-UNROLL2_MAX_OPS = 60
 
 
 def _coef_expr(kind: int, d: int, side_swap: bool) -> str:

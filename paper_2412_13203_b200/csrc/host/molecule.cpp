@@ -2,8 +2,8 @@
 // Restates the reference's input semantics (molecule.hpp:105-158 parse_xyz,
 // basis_set.hpp:33-84 BasisSetTable::parse, basis_set.hpp:112-155
 // attach_basis) so that shells and coefficients are bit-identical to the
-// reference's for the same text (checked by tests/test_boundary.py against
-// oracle/_ref).
+// reference's for the same text (checked by tests/test_abi.py and
+// tests/test_oracle_pins.py against the oracle and oracle/_ref).
 #include "molecule.h"
 
 #include <cctype>

@@ -47,6 +47,41 @@ struct CoopSmem {
   }
 };
 
+// One level of the plan: ops [o0, o1) dealt to this thread with stride `step`.
+// The next op's table entry is loaded while the current one is evaluated (the
+// entry loads were the top long-scoreboard stall of the interpreter, ncu
+// profiles/r02_ncu_coop.txt). lo ops: 2 uint4 per op (up to 5 terms);
+// up ops: 1 uint4 (up to 3 terms).
+template <bool LO>
+__device__ __forceinline__ void coop_level(const uint4* __restrict__ tab, int o0, int o1, int step,
+                                           const double* cf, double* val) {
+  int o = o0;
+  if (o >= o1) return;
+  uint4 h = __ldg(tab + (LO ? 2 * o : o));
+  uint4 g = LO ? __ldg(tab + 2 * o + 1) : make_uint4(0, 0, 0, 0);
+  while (true) {
+    const int on = o + step;
+    uint4 hn = h, gn = g;
+    if (on < o1) {
+      hn = __ldg(tab + (LO ? 2 * on : on));
+      if (LO) gn = __ldg(tab + 2 * on + 1);
+    }
+    const int nt = h.x >> 16;
+    double acc = cf[h.y >> 16] * val[h.y & 0xffff];
+    if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
+    if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
+    if (LO && nt > 3) {
+      acc = fma(cf[g.x >> 16], val[g.x & 0xffff], acc);
+      if (nt > 4) acc = fma(cf[g.y >> 16], val[g.y & 0xffff], acc);
+    }
+    val[h.x & 0xffff] = acc;
+    if (on >= o1) break;
+    o = on;
+    h = hn;
+    g = gn;
+  }
+}
+
 // Evaluate one contracted quartet; outputs end in val[tgt[k]], kernel order.
 template <class C>
 __device__ __forceinline__ void coop_eval(const CoopTables& tb, const PairMeta& bm, const PairMeta& km,
@@ -99,21 +134,8 @@ __device__ __forceinline__ void coop_eval(const CoopTables& tb, const PairMeta& 
     __syncthreads();
     // primitive segment, level by level
     for (int L = 0; L < tb.nlo_lvl; ++L) {
-      const int e = __ldg(tb.lo_lvl + L + 1);
-      for (int o = __ldg(tb.lo_lvl + L) + tid; o < e; o += C::NT) {
-        const uint4* op = reinterpret_cast<const uint4*>(tb.lo) + 2 * o;
-        const uint4 h = __ldg(op);
-        const int nt = h.x >> 16;
-        double acc = cf[h.y >> 16] * val[h.y & 0xffff];
-        if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
-        if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
-        if (nt > 3) {
-          const uint4 g = __ldg(op + 1);
-          acc = fma(cf[g.x >> 16], val[g.x & 0xffff], acc);
-          if (nt > 4) acc = fma(cf[g.y >> 16], val[g.y & 0xffff], acc);
-        }
-        val[h.x & 0xffff] = acc;
-      }
+      coop_level<true>(reinterpret_cast<const uint4*>(tb.lo), __ldg(tb.lo_lvl + L) + tid, __ldg(tb.lo_lvl + L + 1),
+                       C::NT, cf, val);
       __syncthreads();
     }
     for (int k = tid; k < tb.nb; k += C::NT) {
@@ -124,15 +146,8 @@ __device__ __forceinline__ void coop_eval(const CoopTables& tb, const PairMeta& 
   }
   // contracted horizontal segment
   for (int L = 0; L < tb.nup_lvl; ++L) {
-    const int e = __ldg(tb.up_lvl + L + 1);
-    for (int o = __ldg(tb.up_lvl + L) + tid; o < e; o += C::NT) {
-      const uint4 h = __ldg(reinterpret_cast<const uint4*>(tb.up) + o);
-      const int nt = h.x >> 16;
-      double acc = cf[h.y >> 16] * val[h.y & 0xffff];
-      if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
-      if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
-      val[h.x & 0xffff] = acc;
-    }
+    coop_level<false>(reinterpret_cast<const uint4*>(tb.up), __ldg(tb.up_lvl + L) + tid, __ldg(tb.up_lvl + L + 1),
+                      C::NT, cf, val);
     __syncthreads();
   }
 }
@@ -337,21 +352,8 @@ __device__ __forceinline__ void coopw_eval(const CoopTables& tb, const PairMeta&
     }
     __syncwarp();
     for (int L = 0; L < tb.nlo_lvl; ++L) {
-      const int e = __ldg(tb.lo_lvl + L + 1);
-      for (int o = __ldg(tb.lo_lvl + L) + lane; o < e; o += 32) {
-        const uint4* op = reinterpret_cast<const uint4*>(tb.lo) + 2 * o;
-        const uint4 h = __ldg(op);
-        const int nt = h.x >> 16;
-        double acc = cf[h.y >> 16] * val[h.y & 0xffff];
-        if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
-        if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
-        if (nt > 3) {
-          const uint4 g = __ldg(op + 1);
-          acc = fma(cf[g.x >> 16], val[g.x & 0xffff], acc);
-          if (nt > 4) acc = fma(cf[g.y >> 16], val[g.y & 0xffff], acc);
-        }
-        val[h.x & 0xffff] = acc;
-      }
+      coop_level<true>(reinterpret_cast<const uint4*>(tb.lo), __ldg(tb.lo_lvl + L) + lane, __ldg(tb.lo_lvl + L + 1),
+                       32, cf, val);
       __syncwarp();
     }
     for (int k = lane; k < tb.nb; k += 32) {
@@ -363,15 +365,8 @@ __device__ __forceinline__ void coopw_eval(const CoopTables& tb, const PairMeta&
   // coefb[kB_AB..] / [kB_CD..] are set per primitive quartet; the
   // horizontal combos only read UNIT, AB and CD, which are quartet constants
   for (int L = 0; L < tb.nup_lvl; ++L) {
-    const int e = __ldg(tb.up_lvl + L + 1);
-    for (int o = __ldg(tb.up_lvl + L) + lane; o < e; o += 32) {
-      const uint4 h = __ldg(reinterpret_cast<const uint4*>(tb.up) + o);
-      const int nt = h.x >> 16;
-      double acc = cf[h.y >> 16] * val[h.y & 0xffff];
-      if (nt > 1) acc = fma(cf[h.z >> 16], val[h.z & 0xffff], acc);
-      if (nt > 2) acc = fma(cf[h.w >> 16], val[h.w & 0xffff], acc);
-      val[h.x & 0xffff] = acc;
-    }
+    coop_level<false>(reinterpret_cast<const uint4*>(tb.up), __ldg(tb.up_lvl + L) + lane, __ldg(tb.up_lvl + L + 1),
+                      32, cf, val);
     __syncwarp();
   }
 }

@@ -176,8 +176,6 @@ __device__ __forceinline__ void boys_eval_m1(double T, const double* __restrict_
 // accumulator; they differ in how bra records are staged in registers:
 //  kLoopPlain     load each record where it is used (compiler schedules);
 //  kLoopPrefetch  next bra record loaded one step ahead (register rotation);
-//  kLoopTwoKet    two ket primitives per step share one bra record; two
-//                 accumulator sets, folded at the end;
 //  kLoopSmemBra   plain loop; when all lanes of the warp share the bra, its
 //                 primitive records are staged once in shared memory (per
 //                 warp, reused while consecutive items keep the bra).
@@ -188,7 +186,7 @@ __device__ __forceinline__ void boys_eval_m1(double T, const double* __restrict_
 //  kLoopSmemBraL1 as kLoopSmemBra, and step j issues an L1 prefetch of the
 //                 ket record of step j+1 (no registers held; ncu showed the
 //                 first use of each ket record as the top long-scoreboard stall).
-constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopTwoKet = 2, kLoopSmemBra = 4, kLoopSmemBraPf = 8,
+constexpr int kLoopPlain = 0, kLoopPrefetch = 1, kLoopSmemBra = 4, kLoopSmemBraPf = 8,
               kLoopSmemBra2K = 16, kLoopSmemBraL1 = 32;
 
 __device__ __forceinline__ void prefetch_l1(const void* p) {
@@ -231,6 +229,41 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
         if (j + 1 < kk) prefetch_l1(ket + (j + 1) * ks);
       const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
       for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
+    }
+  } else if constexpr (STYLE == kLoopSmemBra2K) {
+    typename C::Acc b;
+    C::zero(b);
+    int j = 0;
+    for (; j + 1 < kk; j += 2) {
+      const PrimRec k0 = load_prim<C::KPA>(ket + j * ks);
+      const PrimRec k1 = load_prim<C::KPA>(ket + (j + 1) * ks);
+      for (int i = 0; i < kb; ++i) {
+        const PrimRec bq = load_prim_gen<C::BPA>(bra + i);
+        C::prim(bq, k0, btab, a);
+        C::prim(bq, k1, btab, b);
+      }
+    }
+    if (j < kk) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
+      for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
+    }
+    C::fold(a, b);
+  } else if constexpr (STYLE == kLoopSmemBraPf) {
+    PrimRec kn = load_prim<C::KPA>(ket);
+    for (int j = 0; j < kk; ++j) {
+      const PrimRec kp = kn;
+      if (j + 1 < kk) kn = load_prim<C::KPA>(ket + (j + 1) * ks);
+      for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
+    }
+  } else if constexpr (STYLE == kLoopPrefetch) {
+    for (int j = 0; j < kk; ++j) {
+      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
+      PrimRec bn = load_prim<C::BPA>(bra);
+      for (int i = 0; i < kb; ++i) {
+        const PrimRec bq = bn;
+        bn = load_prim<C::BPA>(bra + (i + 1 < kb ? i + 1 : i));
+        C::prim(bq, kp, btab, a);
+      }
     }
   } else if constexpr (STYLE == kLoopSmemBra2K) {
     typename C::Acc b;

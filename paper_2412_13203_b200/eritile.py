@@ -260,12 +260,21 @@ class Engine:
         return self
 
     # -- executor
-    def build_jk(self, D: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    def build_jk(self, D: np.ndarray, out: Optional[Tuple[np.ndarray, np.ndarray]] = None) -> Tuple[np.ndarray, np.ndarray]:
+        """J, K of density D through eritile_gpu_build_jk (host buffers). ``out``:
+        caller-owned (N, N) float64 C-contiguous arrays to write into (e.g.
+        page-locked ones, for full-rate copies)."""
         N = self.nbf
         D = np.ascontiguousarray(D, dtype=np.float64)
         if D.shape != (N, N):
             raise ValueError(f"density must be {N}x{N}")
-        J, K = np.zeros((N, N)), np.zeros((N, N))
+        if out is None:
+            J, K = np.zeros((N, N)), np.zeros((N, N))
+        else:
+            J, K = out
+            for M in (J, K):
+                if M.shape != (N, N) or M.dtype != np.float64 or not M.flags.c_contiguous:
+                    raise ValueError(f"out arrays must be C-contiguous float64 {N}x{N}")
         self._check(self._lib.eritile_gpu_build_jk(self._h, D, J, K))
         return J, K
 

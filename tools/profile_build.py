@@ -12,10 +12,11 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 from paper_2412_13203_b200.eritile import Engine, read_fixture  # noqa: E402
-from paper_2412_13203_b200.geometry import water_cluster  # noqa: E402
+from paper_2412_13203_b200.geometry import alanine_chain, water_cluster  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--waters", type=int, default=16)
+ap.add_argument("--geom", default="", help="ala<n>: H-(Ala)_n-OH strand instead of the water cluster")
 ap.add_argument("--basis", default="cc-pvdz.txt")
 ap.add_argument("--tau", type=float, default=1e-10)
 ap.add_argument("--builds", type=int, default=2)
@@ -23,7 +24,8 @@ ap.add_argument("--kappa", type=float, default=1e-14)
 ap.add_argument("--tune", action="store_true")
 ap.add_argument("--set", action="append", default=[], help="CLS=VARIANT, e.g. 1000=fam_x768")
 a = ap.parse_args()
-e = Engine(0).load_molecule(water_cluster(a.waters), read_fixture("basis", a.basis)).build_pairs(a.kappa)
+xyz = alanine_chain(int(a.geom[3:])) if a.geom.startswith("ala") else water_cluster(a.waters)
+e = Engine(0).load_molecule(xyz, read_fixture("basis", a.basis)).build_pairs(a.kappa)
 e.set_screening(a.tau)
 N = e.nbf
 rng = np.random.default_rng(0)
