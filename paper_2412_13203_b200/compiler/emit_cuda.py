@@ -289,13 +289,12 @@ def variants(info) -> List[Tuple[str, str]]:
             # + warp-aggregated K-row updates (OPT 16)
             out.append(("strip_a_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 18>"))
             out.append(("strip_a_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768, 18>"))
-            out.append(("strip_ak2_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 26>"))
             # + L1 prefetch of the next ket record / next item's metadata (OPT 32|4)
             out.append(("strip_p_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 54>"))
-            out.append(("strip_p_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768, 54>"))
             # + d-column K updates to global memory (OPT 64)
             out.append(("strip_s_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 82>"))
-            out.append(("strip_s_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768, 82>"))
+            # + dual items: two kets per lane, one loop nest (OPT 128)
+            out.append(("strip_d_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 146>"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
         if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:
@@ -314,10 +313,10 @@ def variants(info) -> List[Tuple[str, str]]:
         out.append(("fstrip_a_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 18>"))
         out.append(("fstrip_ak2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 26>"))
         out.append(("fstrip_p_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 54>"))
-        out.append(("fstrip_p_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 54>"))
         out.append(("fstrip_s_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 82>"))
-        out.append(("fstrip_s_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 82>"))
         out.append(("fstrip_sk2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 90>"))
+        out.append(("fstrip_d_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 146>"))
+        out.append(("fstrip_d_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 146>"))
     assert len(out) <= 32, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 

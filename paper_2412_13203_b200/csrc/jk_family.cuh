@@ -143,6 +143,55 @@ __device__ __forceinline__ void fam_drive(const PrimRec* __restrict__ bra, const
   }
 }
 
+// Two ket units per lane in one loop nest (strip kernels, kStripDual): same
+// unit group (same K and stride); every bra record / weight read from shared
+// memory feeds two independent primitive chains.
+template <class C, int MB, int MK>
+__device__ __forceinline__ void fam_drive_dual(const PrimRec* bra, const double2* bw, int kb,
+                                               const PrimRec* __restrict__ ket1, const double2* __restrict__ kw1,
+                                               const PrimRec* __restrict__ ket2, const double2* __restrict__ kw2,
+                                               int kk, int ks, const double* __restrict__ btab,
+                                               typename C::Acc (&acc1)[MB][MK], typename C::Acc (&acc2)[MB][MK]) {
+#pragma unroll
+  for (int m = 0; m < MB; ++m)
+#pragma unroll
+    for (int n = 0; n < MK; ++n) {
+      C::zero(acc1[m][n]);
+      C::zero(acc2[m][n]);
+    }
+  for (int j = 0; j < kk; ++j) {
+    const PrimRec k1 = load_prim<C::KPA>(ket1 + j * ks);
+    const PrimRec k2 = load_prim<C::KPA>(ket2 + j * ks);
+    const double2 w1 = __ldg(kw1 + j * ks), w2 = __ldg(kw2 + j * ks);
+    typename C::Acc s1[MB], s2[MB];
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      C::zero(s1[m]);
+      C::zero(s2[m]);
+    }
+    for (int i = 0; i < kb; ++i) {
+      const PrimRec bq = load_prim_gen<C::BPA>(bra + i);
+      const double2 wq = bw[i];
+      if constexpr (MB == 2) {
+        C::prim_w(bq, k1, btab, wq.x, wq.y, s1[0], s1[MB - 1]);
+        C::prim_w(bq, k2, btab, wq.x, wq.y, s2[0], s2[MB - 1]);
+      } else {
+        C::prim_w1(bq, k1, btab, wq.x, s1[0]);
+        C::prim_w1(bq, k2, btab, wq.x, s2[0]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      C::axpy(acc1[m][0], w1.x, s1[m]);
+      C::axpy(acc2[m][0], w2.x, s2[m]);
+      if constexpr (MK == 2) {
+        C::axpy(acc1[m][MK - 1], w1.y, s1[m]);
+        C::axpy(acc2[m][MK - 1], w2.y, s2[m]);
+      }
+    }
+  }
+}
+
 // MB / MK: members per bra / ket unit of this launch segment (items are
 // sorted by (MB, MK) within the class, csrc/host/engine.cu set_screening).
 template <class C, int MB, int MK, int MINB, int STYLE, int NT>

@@ -265,61 +265,34 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
         C::prim(bq, kp, btab, a);
       }
     }
-  } else if constexpr (STYLE == kLoopSmemBra2K) {
-    typename C::Acc b;
-    C::zero(b);
-    int j = 0;
-    for (; j + 1 < kk; j += 2) {
-      const PrimRec k0 = load_prim<C::KPA>(ket + j * ks);
-      const PrimRec k1 = load_prim<C::KPA>(ket + (j + 1) * ks);
-      for (int i = 0; i < kb; ++i) {
-        const PrimRec bq = load_prim_gen<C::BPA>(bra + i);
-        C::prim(bq, k0, btab, a);
-        C::prim(bq, k1, btab, b);
-      }
-    }
-    if (j < kk) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
-      for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
-    }
-    C::fold(a, b);
-  } else if constexpr (STYLE == kLoopSmemBraPf) {
-    PrimRec kn = load_prim<C::KPA>(ket);
-    for (int j = 0; j < kk; ++j) {
-      const PrimRec kp = kn;
-      if (j + 1 < kk) kn = load_prim<C::KPA>(ket + (j + 1) * ks);
-      for (int i = 0; i < kb; ++i) C::prim(load_prim_gen<C::BPA>(bra + i), kp, btab, a);
-    }
-  } else if constexpr (STYLE == kLoopPrefetch) {
-    for (int j = 0; j < kk; ++j) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
-      PrimRec bn = load_prim<C::BPA>(bra);
-      for (int i = 0; i < kb; ++i) {
-        const PrimRec bq = bn;
-        bn = load_prim<C::BPA>(bra + (i + 1 < kb ? i + 1 : i));
-        C::prim(bq, kp, btab, a);
-      }
-    }
-  } else if constexpr (STYLE == kLoopTwoKet) {
-    typename C::Acc b;
-    C::zero(b);
-    int j = 0;
-    for (; j + 1 < kk; j += 2) {
-      const PrimRec k0 = load_prim<C::KPA>(ket + j * ks);
-      const PrimRec k1 = load_prim<C::KPA>(ket + (j + 1) * ks);
-      for (int i = 0; i < kb; ++i) {
-        const PrimRec bq = load_prim<C::BPA>(bra + i);
-        C::prim(bq, k0, btab, a);
-        C::prim(bq, k1, btab, b);
-      }
-    }
-    if (j < kk) {
-      const PrimRec kp = load_prim<C::KPA>(ket + j * ks);
-      for (int i = 0; i < kb; ++i) C::prim(load_prim<C::BPA>(bra + i), kp, btab, a);
-    }
-    C::fold(a, b);
   }
   C::finish(a, ABx, ABy, ABz, CDx, CDy, CDz, out);
+}
+
+// Two kets per lane in one loop nest (strip kernels, kStripDual): both kets
+// have the same primitive count kk (same ket group); every bra record read
+// from shared memory feeds two independent primitive chains.
+template <class C>
+__device__ __forceinline__ void eri_drive_dual(const PrimRec* bra, int kb, const PrimRec* __restrict__ ket1,
+                                               const PrimRec* __restrict__ ket2, int kk, int ks, double ABx,
+                                               double ABy, double ABz, double CDx1, double CDy1, double CDz1,
+                                               double CDx2, double CDy2, double CDz2,
+                                               const double* __restrict__ btab, double (&out1)[C::NV],
+                                               double (&out2)[C::NV]) {
+  typename C::Acc a1, a2;
+  C::zero(a1);
+  C::zero(a2);
+  for (int j = 0; j < kk; ++j) {
+    const PrimRec k1 = load_prim<C::KPA>(ket1 + j * ks);
+    const PrimRec k2 = load_prim<C::KPA>(ket2 + j * ks);
+    for (int i = 0; i < kb; ++i) {
+      const PrimRec bq = load_prim_gen<C::BPA>(bra + i);
+      C::prim(bq, k1, btab, a1);
+      C::prim(bq, k2, btab, a2);
+    }
+  }
+  C::finish(a1, ABx, ABy, ABz, CDx1, CDy1, CDz1, out1);
+  C::finish(a2, ABx, ABy, ABz, CDx2, CDy2, CDz2, out2);
 }
 
 // Component normalisation (molecule.hpp:207-213) for L <= 4, x-major order.

@@ -80,8 +80,12 @@ __device__ __forceinline__ void smem_add_batch(double* sK, const int (&idx)[NE],
 // kStripL1Pf: L1 prefetch of the next ket record (kLoopSmemBraL1) and, with
 // kStripItemPf, of the next item's ket metadata and first ket record.
 // kStripSplitK (with kStripAgg): the d-column K updates go to global memory.
+// kStripDual: a warp claims items in pairs and, when both belong to one ket
+// group (same K), runs each lane's two kets in one loop nest - two independent
+// chains per bra record read and both items' load/digest latencies overlapped
+// (ncu: the strip kernels are latency-bound, 0.7 eligible warps per scheduler).
 constexpr int kStripKetPf = 1, kStripCasBatch = 2, kStripItemPf = 4, kStripTwoKet = 8, kStripAgg = 16,
-              kStripL1Pf = 32, kStripSplitK = 64;
+              kStripL1Pf = 32, kStripSplitK = 64, kStripDual = 128;
 
 // Sum x over the lanes of `peers` (lanes with equal key, this lane included);
 // the lowest lane of the group ends with the total. All 32 lanes must call.
@@ -199,7 +203,8 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
     (void)warp;
     // items are claimed in runs of g = a.gran consecutive items (the
     // Workload Allocator's Combine granularity); s_next may overshoot i1
-    const int g = a.gran > 1 ? a.gran : 1;
+    const int g0 = a.gran > 1 ? a.gran : 1;
+    const int g = (OPT & kStripDual) && g0 < 2 ? 2 : g0;
     int lo = 0, hi = 0;  // this warp's claimed, not yet started items
     auto claim = [&]() -> bool {
       int c = 0;
@@ -215,9 +220,212 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       if (claim()) wn = lo++;
       if (wn < st.i1) nxt = a.items[wn];
     }
+    // digestion of one ket per lane (J_ab in registers, J_cd to global, K rows
+    // in shared memory); called once per item, twice for dual items
+    auto digest = [&](const int y, const bool active, double (&acc_v)[MB][MK][C::NV]) {
+        // digestion metadata of this lane's ket: one 64-byte read (no registers
+        // held across the primitive loop; measured slower when loaded up front)
+        KetMeta km;
+        {
+          const int4* kq = reinterpret_cast<const int4*>(a.kmeta + y);
+          int4 q0, q1, q2;
+          double2 q3;
+          asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q0.x), "=r"(q0.y), "=r"(q0.z), "=r"(q0.w) : "l"(kq));
+          asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q1.x), "=r"(q1.y), "=r"(q1.z), "=r"(q1.w) : "l"(kq + 1));
+          asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q2.x), "=r"(q2.y), "=r"(q2.z), "=r"(q2.w) : "l"(kq + 2));
+          asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(q3.x), "=d"(q3.y) : "l"(kq + 3));
+          km.bfa[0] = q0.x; km.bfa[1] = q0.y; km.bfb[0] = q0.z; km.bfb[1] = q0.w;
+          km.colc[0] = q1.x; km.colc[1] = q1.y; km.cold[0] = q1.z; km.cold[1] = q1.w;
+          km.offd[0] = q2.x; km.offd[1] = q2.y; km.m[0] = q2.z; km.m[1] = q2.w;
+          km.q[0] = q3.x; km.q[1] = q3.y;
+        }
+  #pragma unroll
+        for (int m = 0; m < MB; ++m) {
+          PairMeta bm;
+          bm.bfa = s_bm[m][0];
+          bm.bfb = s_bm[m][1];
+          bm.sha = s_bm[m][2];
+          bm.shb = s_bm[m][3];
+          const int rA = st.rowA[m], rB = st.rowB[m];
+  #pragma unroll
+          for (int k = 0; k < MK; ++k) {
+            const int py = km.m[k];
+            bool keep = active;
+            if constexpr (FAM) keep = keep && !(st.bra == y && m > k) && (a.tau <= 0.0 || s_bq[m] * km.q[k] >= a.tau);
+            constexpr bool AGG = (OPT & kStripAgg) != 0;
+            if constexpr (AGG) {  // the whole warp digests (shuffle groups), non-kept lanes add zeros
+              if (!__any_sync(0xffffffffu, keep)) continue;
+            } else {
+              if (!keep) continue;
+            }
+            const int kbfa = km.bfa[k], kbfb = km.bfb[k];
+            const double* v = acc_v[m][k];
+            const double deg =
+                (bm.sha != bm.shb ? 2.0 : 1.0) * (km.offd[k] ? 2.0 : 1.0) * (bpx[m] != py ? 2.0 : 1.0);
+            const double wj = keep ? 0.5 * deg : 0.0, wk = keep ? 0.25 * deg : 0.0;
+            const int colC = km.colc[k];
+            const int colD = km.cold[k] + (LDOFF ? a.ncolC : 0);
+            const double* Dab = a.D + bm.bfa * n + bm.bfb;
+            const double* Dcd = a.D + kbfa * n + kbfb;
+            auto dsm = [&](int row, int col, size_t grow, size_t gcol) -> double {
+              if constexpr (DSM) return sD[row * ncol + col];
+              else return __ldg(a.D + grow * n + gcol);
+            };
+  #pragma unroll
+            for (int ia = 0; ia < C::NA; ++ia)
+  #pragma unroll
+              for (int ib = 0; ib < C::NB; ++ib) {
+                double t = 0.0;
+  #pragma unroll
+                for (int ic = 0; ic < C::NC; ++ic)
+  #pragma unroll
+                  for (int id = 0; id < C::ND; ++id)
+                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dcd + ic * n + id), t);
+                jab[m][ia * C::NB + ib] = fma(t, wj, jab[m][ia * C::NB + ib]);
+              }
+  #pragma unroll
+            for (int ic = 0; ic < C::NC; ++ic)
+  #pragma unroll
+              for (int id = 0; id < C::ND; ++id) {
+                double t = 0.0;
+  #pragma unroll
+                for (int ia = 0; ia < C::NA; ++ia)
+  #pragma unroll
+                  for (int ib = 0; ib < C::NB; ++ib)
+                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), t);
+                if (keep) red_add(a.J + (kbfa + ic) * n + kbfb + id, t * wj, 0);
+              }
+            // K_ac += sum_bd v D_bd ; K_ad += sum_bc v D_bc   (rows a of the bra)
+            // K_bd += sum_ac v D_ac ; K_bc += sum_ad v D_ad   (rows b of the bra)
+            constexpr int NKE = C::NA * (C::NC + C::ND) + C::NB * (C::NC + C::ND);
+            int kidx[NKE];
+            double kval[NKE];
+            int ne = 0;
+  #pragma unroll
+            for (int ia = 0; ia < C::NA; ++ia) {
+  #pragma unroll
+              for (int ic = 0; ic < C::NC; ++ic) {
+                double t = 0.0;
+  #pragma unroll
+                for (int ib = 0; ib < C::NB; ++ib)
+  #pragma unroll
+                  for (int id = 0; id < C::ND; ++id)
+                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                            dsm(rB + ib, colD + id, bm.bfb + ib, kbfb + id), t);
+                kidx[ne] = (rA + ia) * ncol + colC + ic;
+                kval[ne++] = t * wk;
+              }
+  #pragma unroll
+              for (int id = 0; id < C::ND; ++id) {
+                double t = 0.0;
+  #pragma unroll
+                for (int ib = 0; ib < C::NB; ++ib)
+  #pragma unroll
+                  for (int ic = 0; ic < C::NC; ++ic)
+                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                            dsm(rB + ib, colC + ic, bm.bfb + ib, kbfa + ic), t);
+                kidx[ne] = (rA + ia) * ncol + colD + id;
+                kval[ne++] = t * wk;
+              }
+            }
+  #pragma unroll
+            for (int ib = 0; ib < C::NB; ++ib) {
+  #pragma unroll
+              for (int id = 0; id < C::ND; ++id) {
+                double t = 0.0;
+  #pragma unroll
+                for (int ia = 0; ia < C::NA; ++ia)
+  #pragma unroll
+                  for (int ic = 0; ic < C::NC; ++ic)
+                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                            dsm(rA + ia, colC + ic, bm.bfa + ia, kbfa + ic), t);
+                kidx[ne] = (rB + ib) * ncol + colD + id;
+                kval[ne++] = t * wk;
+              }
+  #pragma unroll
+              for (int ic = 0; ic < C::NC; ++ic) {
+                double t = 0.0;
+  #pragma unroll
+                for (int ia = 0; ia < C::NA; ++ia)
+  #pragma unroll
+                  for (int id = 0; id < C::ND; ++id)
+                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
+                            dsm(rA + ia, colD + id, bm.bfa + ia, kbfb + id), t);
+                kidx[ne] = (rB + ib) * ncol + colC + ic;
+                kval[ne++] = t * wk;
+              }
+            }
+            if constexpr (AGG) {
+              // c-keyed updates (K_ac, K_bc) and d-keyed updates (K_ad, K_bd)
+              constexpr int NCK = (C::NA + C::NB) * C::NC, NDK = (C::NA + C::NB) * C::ND;
+              int ci[NCK], di[NDK];
+              double cv[NCK], dv[NDK];
+              int nc = 0, nd = 0;
+  #pragma unroll
+              for (int ia = 0; ia < C::NA; ++ia) {
+  #pragma unroll
+                for (int ic = 0; ic < C::NC; ++ic) {
+                  ci[nc] = kidx[ia * (C::NC + C::ND) + ic];
+                  cv[nc++] = kval[ia * (C::NC + C::ND) + ic];
+                }
+  #pragma unroll
+                for (int id = 0; id < C::ND; ++id) {
+                  di[nd] = kidx[ia * (C::NC + C::ND) + C::NC + id];
+                  dv[nd++] = kval[ia * (C::NC + C::ND) + C::NC + id];
+                }
+              }
+  #pragma unroll
+              for (int ib = 0; ib < C::NB; ++ib) {
+                constexpr int b0 = C::NA * (C::NC + C::ND);
+  #pragma unroll
+                for (int id = 0; id < C::ND; ++id) {
+                  di[nd] = kidx[b0 + ib * (C::NC + C::ND) + id];
+                  dv[nd++] = kval[b0 + ib * (C::NC + C::ND) + id];
+                }
+  #pragma unroll
+                for (int ic = 0; ic < C::NC; ++ic) {
+                  ci[nc] = kidx[b0 + ib * (C::NC + C::ND) + C::ND + ic];
+                  cv[nc++] = kval[b0 + ib * (C::NC + C::ND) + C::ND + ic];
+                }
+              }
+              const unsigned pc = __match_any_sync(0xffffffffu, keep ? colC : -1 - lane);
+              const unsigned pd = __match_any_sync(0xffffffffu, keep ? colD : -1 - lane);
+              reduce_peers<NCK>(pc, cv, lane);
+              reduce_peers<NDK>(pd, dv, lane);
+              if (keep && __ffs(pc) - 1 == lane) smem_add_batch<NCK>(sK, ci, cv);
+              if (keep && __ffs(pd) - 1 == lane) {
+                if constexpr (OPT & kStripSplitK) {
+                  // d-column updates straight to global K (L2 RED.ADD.F64): the
+                  // shared-memory atomic unit (~2 cycles per lane) and the L2
+                  // atomic units then each carry half of the K traffic
+                  int e = 0;
+  #pragma unroll
+                  for (int ia = 0; ia < C::NA; ++ia)
+  #pragma unroll
+                    for (int id = 0; id < C::ND; ++id)
+                      red_add(a.K + (bm.bfa + ia) * n + kbfb + id, dv[e++], 0);
+  #pragma unroll
+                  for (int ib = 0; ib < C::NB; ++ib)
+  #pragma unroll
+                    for (int id = 0; id < C::ND; ++id)
+                      red_add(a.K + (bm.bfb + ib) * n + kbfb + id, dv[e++], 0);
+                } else {
+                  smem_add_batch<NDK>(sK, di, dv);
+                }
+              }
+            } else if constexpr (OPT & kStripCasBatch) {
+              smem_add_batch<NKE>(sK, kidx, kval);
+            } else {
+  #pragma unroll
+              for (int e = 0; e < NKE; ++e) atomicAdd(sK + kidx[e], kval[e]);
+            }
+          }
+        }
+    };
     for (;;) {
       int w = 0;
-      WorkItem it;
+      WorkItem it, it2{};
+      bool dual = false;  // kStripDual: two consecutive items of one ket group
       if constexpr (OPT & kStripItemPf) {
         w = wn;
         if (w >= st.i1) break;
@@ -229,19 +437,51 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         if (lo >= hi && !claim()) break;
         w = lo++;
         it = a.items[w];
+        if constexpr (OPT & kStripDual) {
+          if (lo < hi) {
+            it2 = a.items[lo];
+            dual = it2.yfirst == it.yfirst;
+            if (dual) ++lo;
+          }
+        }
       }
       (void)w;
+      (void)dual;
       const int nq = it.r0nq >> 24;
       const bool active = lane < nq;
       const int y = it.yfirst + (it.r0nq & 0xffffff) + (active ? lane : 0);  // single-bra item
+      const int nq2 = it2.r0nq >> 24;
+      const bool active2 = dual && lane < nq2;
+      const int y2 = dual ? it2.yfirst + (it2.r0nq & 0xffffff) + (active2 ? lane : 0) : y;
+      (void)y2;
       double acc_v[MB][MK][C::NV];
+      double acc_v2[(OPT & kStripDual) ? MB : 1][(OPT & kStripDual) ? MK : 1][C::NV];
       (void)acc_v;
+      (void)acc_v2;
       double ABx, ABy, ABz, CDx, CDy, CDz;
       if constexpr (FAM) {
         const UnitMeta ku = a.um[y];
         ABx = s_bab[0]; ABy = s_bab[1]; ABz = s_bab[2];
         CDx = ku.ABx; CDy = ku.ABy; CDz = ku.ABz;
         typename C::Acc acc[MB][MK];
+        if constexpr (OPT & kStripDual) {
+          if (dual) {  // both kets of the lane in one loop nest: two chains per bra record read
+            const UnitMeta ku2 = a.um[y2];
+            typename C::Acc acc2[MB][MK];
+            fam_drive_dual<C, MB, MK>(brap, bwp, kb, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, a.ukprims + ku2.ksoa,
+                                      a.ukw + ku2.ksoa, ku.K, ku.kstride, smem, acc, acc2);
+#pragma unroll
+            for (int m = 0; m < MB; ++m)
+#pragma unroll
+              for (int k = 0; k < MK; ++k) {
+                C::finish(acc[m][k], ABx, ABy, ABz, CDx, CDy, CDz, acc_v[m][k]);
+                C::finish(acc2[m][k], ABx, ABy, ABz, ku2.ABx, ku2.ABy, ku2.ABz, acc_v2[m][k]);
+              }
+            digest(y, active, acc_v);
+            digest(y2, active2, acc_v2);
+            continue;
+          }
+        }
 #if ERITILE_PROBE_STRIP == 2  // measurement build: no primitive loop
         fam_drive<C, MB, MK, kLoop>(brap, bwp, kb, a.ukprims + ku.ksoa, a.ukw + ku.ksoa, 0,
 #else
@@ -259,6 +499,18 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
         CDx = cd.x; CDy = cd.y; CDz = __ldg(&a.pm[y].ABz);
         const int2 ks = __ldg(reinterpret_cast<const int2*>(&a.pm[y].ksoa));
         const int kstride = __ldg(&a.pm[y].kstride);
+        if constexpr (OPT & kStripDual) {
+          if (dual) {
+            const int ks2 = __ldg(&a.pm[y2].ksoa);
+            const double2 cd2 = __ldg(reinterpret_cast<const double2*>(&a.pm[y2].ABx));
+            const double cdz2 = __ldg(&a.pm[y2].ABz);
+            eri_drive_dual<C>(brap, kb, a.kprims + ks.x, a.kprims + ks2, kh.y, kstride, ABx, ABy, ABz, CDx, CDy,
+                              CDz, cd2.x, cd2.y, cdz2, smem, acc_v[0][0], acc_v2[0][0]);
+            digest(y, active, acc_v);
+            digest(y2, active2, acc_v2);
+            continue;
+          }
+        }
         eri_drive<C, kLoop>(brap, kb, a.kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy,
                                    CDz, smem, acc_v[0][0]);
       }
@@ -284,204 +536,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
           else prefetch_l1(a.pm + yn);
         }
       }
-      // digestion metadata of this lane's ket: one 64-byte read (no registers
-      // held across the primitive loop; measured slower when loaded up front)
-      KetMeta km;
-      {
-        const int4* kq = reinterpret_cast<const int4*>(a.kmeta + y);
-        int4 q0, q1, q2;
-        double2 q3;
-        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q0.x), "=r"(q0.y), "=r"(q0.z), "=r"(q0.w) : "l"(kq));
-        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q1.x), "=r"(q1.y), "=r"(q1.z), "=r"(q1.w) : "l"(kq + 1));
-        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(q2.x), "=r"(q2.y), "=r"(q2.z), "=r"(q2.w) : "l"(kq + 2));
-        asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(q3.x), "=d"(q3.y) : "l"(kq + 3));
-        km.bfa[0] = q0.x; km.bfa[1] = q0.y; km.bfb[0] = q0.z; km.bfb[1] = q0.w;
-        km.colc[0] = q1.x; km.colc[1] = q1.y; km.cold[0] = q1.z; km.cold[1] = q1.w;
-        km.offd[0] = q2.x; km.offd[1] = q2.y; km.m[0] = q2.z; km.m[1] = q2.w;
-        km.q[0] = q3.x; km.q[1] = q3.y;
-      }
-#pragma unroll
-      for (int m = 0; m < MB; ++m) {
-        PairMeta bm;
-        bm.bfa = s_bm[m][0];
-        bm.bfb = s_bm[m][1];
-        bm.sha = s_bm[m][2];
-        bm.shb = s_bm[m][3];
-        const int rA = st.rowA[m], rB = st.rowB[m];
-#pragma unroll
-        for (int k = 0; k < MK; ++k) {
-          const int py = km.m[k];
-          bool keep = active;
-          if constexpr (FAM) keep = keep && !(st.bra == y && m > k) && (a.tau <= 0.0 || s_bq[m] * km.q[k] >= a.tau);
-          constexpr bool AGG = (OPT & kStripAgg) != 0;
-          if constexpr (AGG) {  // the whole warp digests (shuffle groups), non-kept lanes add zeros
-            if (!__any_sync(0xffffffffu, keep)) continue;
-          } else {
-            if (!keep) continue;
-          }
-          const int kbfa = km.bfa[k], kbfb = km.bfb[k];
-          const double* v = acc_v[m][k];
-          const double deg =
-              (bm.sha != bm.shb ? 2.0 : 1.0) * (km.offd[k] ? 2.0 : 1.0) * (bpx[m] != py ? 2.0 : 1.0);
-          const double wj = keep ? 0.5 * deg : 0.0, wk = keep ? 0.25 * deg : 0.0;
-          const int colC = km.colc[k];
-          const int colD = km.cold[k] + (LDOFF ? a.ncolC : 0);
-          const double* Dab = a.D + bm.bfa * n + bm.bfb;
-          const double* Dcd = a.D + kbfa * n + kbfb;
-          auto dsm = [&](int row, int col, size_t grow, size_t gcol) -> double {
-            if constexpr (DSM) return sD[row * ncol + col];
-            else return __ldg(a.D + grow * n + gcol);
-          };
-#pragma unroll
-          for (int ia = 0; ia < C::NA; ++ia)
-#pragma unroll
-            for (int ib = 0; ib < C::NB; ++ib) {
-              double t = 0.0;
-#pragma unroll
-              for (int ic = 0; ic < C::NC; ++ic)
-#pragma unroll
-                for (int id = 0; id < C::ND; ++id)
-                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dcd + ic * n + id), t);
-              jab[m][ia * C::NB + ib] = fma(t, wj, jab[m][ia * C::NB + ib]);
-            }
-#pragma unroll
-          for (int ic = 0; ic < C::NC; ++ic)
-#pragma unroll
-            for (int id = 0; id < C::ND; ++id) {
-              double t = 0.0;
-#pragma unroll
-              for (int ia = 0; ia < C::NA; ++ia)
-#pragma unroll
-                for (int ib = 0; ib < C::NB; ++ib)
-                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), t);
-              if (keep) red_add(a.J + (kbfa + ic) * n + kbfb + id, t * wj, 0);
-            }
-          // K_ac += sum_bd v D_bd ; K_ad += sum_bc v D_bc   (rows a of the bra)
-          // K_bd += sum_ac v D_ac ; K_bc += sum_ad v D_ad   (rows b of the bra)
-          constexpr int NKE = C::NA * (C::NC + C::ND) + C::NB * (C::NC + C::ND);
-          int kidx[NKE];
-          double kval[NKE];
-          int ne = 0;
-#pragma unroll
-          for (int ia = 0; ia < C::NA; ++ia) {
-#pragma unroll
-            for (int ic = 0; ic < C::NC; ++ic) {
-              double t = 0.0;
-#pragma unroll
-              for (int ib = 0; ib < C::NB; ++ib)
-#pragma unroll
-                for (int id = 0; id < C::ND; ++id)
-                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rB + ib, colD + id, bm.bfb + ib, kbfb + id), t);
-              kidx[ne] = (rA + ia) * ncol + colC + ic;
-              kval[ne++] = t * wk;
-            }
-#pragma unroll
-            for (int id = 0; id < C::ND; ++id) {
-              double t = 0.0;
-#pragma unroll
-              for (int ib = 0; ib < C::NB; ++ib)
-#pragma unroll
-                for (int ic = 0; ic < C::NC; ++ic)
-                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rB + ib, colC + ic, bm.bfb + ib, kbfa + ic), t);
-              kidx[ne] = (rA + ia) * ncol + colD + id;
-              kval[ne++] = t * wk;
-            }
-          }
-#pragma unroll
-          for (int ib = 0; ib < C::NB; ++ib) {
-#pragma unroll
-            for (int id = 0; id < C::ND; ++id) {
-              double t = 0.0;
-#pragma unroll
-              for (int ia = 0; ia < C::NA; ++ia)
-#pragma unroll
-                for (int ic = 0; ic < C::NC; ++ic)
-                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rA + ia, colC + ic, bm.bfa + ia, kbfa + ic), t);
-              kidx[ne] = (rB + ib) * ncol + colD + id;
-              kval[ne++] = t * wk;
-            }
-#pragma unroll
-            for (int ic = 0; ic < C::NC; ++ic) {
-              double t = 0.0;
-#pragma unroll
-              for (int ia = 0; ia < C::NA; ++ia)
-#pragma unroll
-                for (int id = 0; id < C::ND; ++id)
-                  t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id],
-                          dsm(rA + ia, colD + id, bm.bfa + ia, kbfb + id), t);
-              kidx[ne] = (rB + ib) * ncol + colC + ic;
-              kval[ne++] = t * wk;
-            }
-          }
-          if constexpr (AGG) {
-            // c-keyed updates (K_ac, K_bc) and d-keyed updates (K_ad, K_bd)
-            constexpr int NCK = (C::NA + C::NB) * C::NC, NDK = (C::NA + C::NB) * C::ND;
-            int ci[NCK], di[NDK];
-            double cv[NCK], dv[NDK];
-            int nc = 0, nd = 0;
-#pragma unroll
-            for (int ia = 0; ia < C::NA; ++ia) {
-#pragma unroll
-              for (int ic = 0; ic < C::NC; ++ic) {
-                ci[nc] = kidx[ia * (C::NC + C::ND) + ic];
-                cv[nc++] = kval[ia * (C::NC + C::ND) + ic];
-              }
-#pragma unroll
-              for (int id = 0; id < C::ND; ++id) {
-                di[nd] = kidx[ia * (C::NC + C::ND) + C::NC + id];
-                dv[nd++] = kval[ia * (C::NC + C::ND) + C::NC + id];
-              }
-            }
-#pragma unroll
-            for (int ib = 0; ib < C::NB; ++ib) {
-              constexpr int b0 = C::NA * (C::NC + C::ND);
-#pragma unroll
-              for (int id = 0; id < C::ND; ++id) {
-                di[nd] = kidx[b0 + ib * (C::NC + C::ND) + id];
-                dv[nd++] = kval[b0 + ib * (C::NC + C::ND) + id];
-              }
-#pragma unroll
-              for (int ic = 0; ic < C::NC; ++ic) {
-                ci[nc] = kidx[b0 + ib * (C::NC + C::ND) + C::ND + ic];
-                cv[nc++] = kval[b0 + ib * (C::NC + C::ND) + C::ND + ic];
-              }
-            }
-            const unsigned pc = __match_any_sync(0xffffffffu, keep ? colC : -1 - lane);
-            const unsigned pd = __match_any_sync(0xffffffffu, keep ? colD : -1 - lane);
-            reduce_peers<NCK>(pc, cv, lane);
-            reduce_peers<NDK>(pd, dv, lane);
-            if (keep && __ffs(pc) - 1 == lane) smem_add_batch<NCK>(sK, ci, cv);
-            if (keep && __ffs(pd) - 1 == lane) {
-              if constexpr (OPT & kStripSplitK) {
-                // d-column updates straight to global K (L2 RED.ADD.F64): the
-                // shared-memory atomic unit (~2 cycles per lane) and the L2
-                // atomic units then each carry half of the K traffic
-                int e = 0;
-#pragma unroll
-                for (int ia = 0; ia < C::NA; ++ia)
-#pragma unroll
-                  for (int id = 0; id < C::ND; ++id)
-                    red_add(a.K + (bm.bfa + ia) * n + kbfb + id, dv[e++], 0);
-#pragma unroll
-                for (int ib = 0; ib < C::NB; ++ib)
-#pragma unroll
-                  for (int id = 0; id < C::ND; ++id)
-                    red_add(a.K + (bm.bfb + ib) * n + kbfb + id, dv[e++], 0);
-              } else {
-                smem_add_batch<NDK>(sK, di, dv);
-              }
-            }
-          } else if constexpr (OPT & kStripCasBatch) {
-            smem_add_batch<NKE>(sK, kidx, kval);
-          } else {
-#pragma unroll
-            for (int e = 0; e < NKE; ++e) atomicAdd(sK + kidx[e], kval[e]);
-          }
-        }
-      }
+      digest(y, active, acc_v);
     }
     // J_ab: one butterfly per strip and warp, one RED per element and warp
 #pragma unroll
