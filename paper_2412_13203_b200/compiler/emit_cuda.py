@@ -248,6 +248,10 @@ def emit_class(cls) -> Tuple[str, Dict]:
 # flavours for the small plans; CTA-cooperative table kernels (compiler/
 # coop.py) for plans of at least COOP_MIN_OPS operations.
 LANE_MAX_OPS = int(os.environ.get("ERITILE_LANE_MAX_OPS", "4000"))
+# d/f classes above LANE_MAX_OPS (cc-pVTZ, config 5) also get one straight-line
+# lane variant at the 255-register budget (values beyond the register file
+# live in the thread's local memory): 1-3 minutes of nvcc per class
+LANE_BIG_MAX_OPS = int(os.environ.get("ERITILE_LANE_BIG_MAX_OPS", "13000"))
 COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2, 3)
@@ -295,6 +299,9 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("strip_s_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 82>"))
             # + dual items: two kets per lane, one loop nest (OPT 128)
             out.append(("strip_d_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 146>"))
+    elif info["ops"] <= LANE_BIG_MAX_OPS and info["ops"] >= COOP_MIN_OPS:
+        # J/K only; the Schwarz / raw-quartet modes go to the coop kernel
+        out.append(("lane_plm1", f"launch_big_lane_cls{cid}"))
     if info["ops"] >= COOP_MIN_OPS:
         out.append(("coop", f"launch_coop_cls{cid}"))
         if info.get("coop_slots", 1 << 30) <= COOPW_MAX_SLOTS:
@@ -393,6 +400,11 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
                            f"t.nslots = {sc['nslots']}; t.tgt0 = {sc['tgt'][0]};")
                 src.append(f"  launch_coopw<CoopCls{cid}>(t, a);")
                 src.append("}")
+        if any(expr == f"launch_big_lane_cls{cid}" for _, expr in vs):
+            src.append(f"void launch_big_lane_cls{cid}(const LaunchArgs& a) {{")
+            src.append(f"  if (a.mode != 0) return launch_coop_cls{cid}(a);")
+            src.append(f"  launch_class<Cls{cid}, 1, kLoopPlain, kJkThreads, true>(a);")
+            src.append("}")
         for name, expr in vs:
             if name not in ("coop", "coopw"):
                 src.append(f"void launch_{name}_cls{cid}(const LaunchArgs& a) {{ {expr}(a); }}")

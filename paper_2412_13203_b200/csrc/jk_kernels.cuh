@@ -679,7 +679,10 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 // NT: threads per CTA. One Boys slice is staged per CTA, so 512/768-thread
 // CTAs at MINB = 1 keep 16/24 warps per SM with a single 51 KB table and
 // leave the rest of the 256 KB L1/shared array to L1 (primitive records).
-template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
+// JK_ONLY: only the J/K kernel is instantiated (the Schwarz / raw-quartet
+// modes of the big d/f classes run on their coop kernel instead: each
+// instantiation of the straight-line plan costs minutes of nvcc).
+template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads, bool JK_ONLY = false>
 void launch_class(const LaunchArgs& a) {
   const size_t smem = BoysStage<C>::bytes +
                       (STYLE == kLoopSmemBra && a.mode == 0 ? sizeof(PrimRec) * kSmemBraMax * (NT / 32) : 0);
@@ -694,6 +697,8 @@ void launch_class(const LaunchArgs& a) {
     const int grid = a.grid > 0 ? a.grid : static_cast<int>(want < cap ? want : cap);
     jk_kernel<C, MINB, STYLE, NT><<<grid, NT, smem, a.stream>>>(a.items, a.nitems, a.cnt, a.pm, a.prims, a.D, a.J,
                                                        a.K, a.N, a.boys_tab, a.kprims, a.det, a.gran);
+  } else if constexpr (JK_ONLY) {
+    return;  // (callers route modes 1 and 2 elsewhere)
   } else if (a.mode == 2) {
     if (a.nq <= 0) return;
     cudaFuncSetAttribute(quartet_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
