@@ -160,20 +160,20 @@ def fp64_peak():
     return FP64_DATASHEET_TFLOPS, "fallback: B200 datasheet FP64 (148 SM x 64 DFMA x 2 x 1.965 GHz)"
 
 
-def ncu_traffic(workload: str, kernel: str):
-    """DRAM bytes (read + write) per launch of the dominant kernel from an
-    `ncu --set full` capture of the same workload and kernel variant on the
-    current tree (profiles/ncu_traffic.json, written by tools/ncu_traffic.sh).
-    None when no capture matches this run's workload and kernel."""
+def ncu_traffic(workload: str, cls: str):
+    """DRAM bytes (read + write) of the dominant class launch (all its kernels)
+    from an ncu capture of the same workload and class on the current tree
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.sh, which names
+    the kernel variant it measured). None when no capture matches."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         try:
             for d in json.loads(p.read_text()):
-                if d.get("workload") == workload and d.get("kernel") == kernel:
+                if d.get("workload") == workload and d.get("cls") == cls:
                     return d.get("dram_bytes_per_launch"), d.get("source")
         except Exception:
             pass
-    return None, "no ncu capture of this workload/kernel on the current tree"
+    return None, "no ncu capture of this workload/class on the current tree"
 
 
 # ------------------------------------------------------------------ CPU arm
@@ -419,7 +419,7 @@ def run_ours(args, rank, nranks, local_rank):
     if top:
         ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
         kern = "class (%d%d%d%d) launch, variant %s" % (*top["cls"], chosen.get(tuple(top["cls"])))
-        traffic, traffic_src = ncu_traffic(config(args, 1)["workload"], kern)
+        traffic, traffic_src = ncu_traffic(config(args, 1)["workload"], "".join(map(str, top["cls"])))
         roof = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                 "frac_vs_datasheet": ach / FP64_DATASHEET_TFLOPS,
                 "traffic": traffic, "traffic_source": traffic_src,

@@ -1,4 +1,4 @@
-O=gpurun_out/r02_u; mkdir -p $O
+O=gpurun_out/r02_v; mkdir -p $O
 timeout 1200 python -m pytest tests/test_gpu_c5.py tests/test_gpu_parity.py -q -x  > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
 tail -3 $O/pytest.log
 timeout 1200 python bench.py --geom ala4 --basis cc-pvtz --no-unscreened --no-cpu --steps 3 --warmup 3 > $O/bench_ala4.json 2> $O/bench_ala4.err

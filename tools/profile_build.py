@@ -23,6 +23,9 @@ ap.add_argument("--builds", type=int, default=2)
 ap.add_argument("--kappa", type=float, default=1e-14)
 ap.add_argument("--tune", action="store_true")
 ap.add_argument("--set", action="append", default=[], help="CLS=VARIANT, e.g. 1000=fam_x768")
+ap.add_argument("--variants-json", default="", help="write {class: chosen variant} here")
+ap.add_argument("--profile-range", action="store_true",
+                help="cudaProfilerStart/Stop around the measured builds only (ncu --profile-from-start off)")
 a = ap.parse_args()
 xyz = alanine_chain(int(a.geom[3:])) if a.geom.startswith("ala") else water_cluster(a.waters)
 e = Engine(0).load_molecule(xyz, read_fixture("basis", a.basis)).build_pairs(a.kappa)
@@ -40,6 +43,17 @@ if a.set:
     for kv in a.set:
         c, v = kv.split("=")
         e.set_variant(tab.index(c), v)
+if a.variants_json:
+    import json
+    json.dump({"".join(map(str, k[:4])) if not isinstance(k, str) else k: v for k, v in e.variants().items()},
+              open(a.variants_json, "w"))
+if a.profile_range:
+    import torch
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
 for _ in range(a.builds):
     J, K = e.build_jk(D)
+if a.profile_range:
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 print(e.stats())
