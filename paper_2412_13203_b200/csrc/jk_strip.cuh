@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
   __shared__ int s_next;                              // next item of the strip (dynamic hand-out)
   __shared__ double s_bq[MB];                         // Schwarz Q of the bra members
   __shared__ double s_bab[3];                         // bra AB vector
+  __shared__ double s_dab[MB][C::NA * C::NB];         // D'_ab of the bra members (J_cd)
   (void)sD;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
@@ -172,6 +173,14 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       } else {
         s_bab[0] = a.pm[st.bra].ABx; s_bab[1] = a.pm[st.bra].ABy; s_bab[2] = a.pm[st.bra].ABz;
       }
+    }
+    for (int e = threadIdx.x; e < MB * C::NA * C::NB; e += NT) {
+      // (the bra members' first functions, read from global: s_bm is not yet visible)
+      const int m = e / (C::NA * C::NB), ab = e % (C::NA * C::NB);
+      int px = st.bra;
+      if constexpr (FAM) px = m == 0 ? a.um[st.bra].m0 : a.um[st.bra].m1;
+      const int bfa = __ldg(&a.pm[px].bfa), bfb = __ldg(&a.pm[px].bfb);
+      s_dab[m][ab] = __ldg(a.D + static_cast<size_t>(bfa + ab / C::NB) * n + bfb + ab % C::NB);
     }
     if (threadIdx.x == 0) s_next = st.i0;
     for (int e = threadIdx.x; e < nrows * ncol; e += NT) sK[e] = 0.0;
@@ -265,7 +274,6 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
             const double wj = keep ? 0.5 * deg : 0.0, wk = keep ? 0.25 * deg : 0.0;
             const int colC = km.colc[k];
             const int colD = km.cold[k] + (LDOFF ? a.ncolC : 0);
-            const double* Dab = a.D + bm.bfa * n + bm.bfb;
             const double* Dcd = a.D + kbfa * n + kbfb;
             auto dsm = [&](int row, int col, size_t grow, size_t gcol) -> double {
               if constexpr (DSM) return sD[row * ncol + col];
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
                 for (int ia = 0; ia < C::NA; ++ia)
   #pragma unroll
                   for (int ib = 0; ib < C::NB; ++ib)
-                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], __ldg(Dab + ia * n + ib), t);
+                    t = fma(v[((ia * C::NB + ib) * C::NC + ic) * C::ND + id], s_dab[m][ia * C::NB + ib], t);
                 if (keep) red_add(a.J + (kbfa + ic) * n + kbfb + id, t * wj, 0);
               }
             // K_ac += sum_bd v D_bd ; K_ad += sum_bc v D_bc   (rows a of the bra)
@@ -450,9 +458,11 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
       const int nq = it.r0nq >> 24;
       const bool active = lane < nq;
       const int y = it.yfirst + (it.r0nq & 0xffffff) + (active ? lane : 0);  // single-bra item
+      prefetch_l1(a.kmeta + y);  // read again after the primitive loop (digestion)
       const int nq2 = it2.r0nq >> 24;
       const bool active2 = dual && lane < nq2;
       const int y2 = dual ? it2.yfirst + (it2.r0nq & 0xffffff) + (active2 ? lane : 0) : y;
+      if (dual) prefetch_l1(a.kmeta + y2);
       (void)y2;
       double acc_v[MB][MK][C::NV];
       double acc_v2[(OPT & kStripDual) ? MB : 1][(OPT & kStripDual) ? MK : 1][C::NV];

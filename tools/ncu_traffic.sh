@@ -3,10 +3,12 @@
 # every kernel of class CLS (default 1000, (ps|ss)) in one tuned (H2O)_80 build,
 # dram__bytes_read/write summed over the class's launches -> profiles/ncu_traffic.json
 CLS=${1:-1000}
+VAR=${2:-}   # kernel variant to measure (default: whatever --tune picks)
+SET=""; [ -n "$VAR" ] && SET="--set $CLS=$VAR"
 O=gpurun_out/traffic_$CLS; mkdir -p $O
 timeout 1200 ncu --profile-from-start off --clock-control none --kernel-name-base demangled -k "regex:Cls$CLS," \
   --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file $O/traffic.csv \
-  python tools/profile_build.py --waters 80 --builds 1 --tune --profile-range --variants-json $O/variants.json > $O/log.txt 2>&1
+  python tools/profile_build.py --waters 80 --builds 1 --tune $SET --profile-range --variants-json $O/variants.json > $O/log.txt 2>&1
 python - "$O" "$CLS" <<'PY'
 import csv, json, sys
 O, cls = sys.argv[1], sys.argv[2]
