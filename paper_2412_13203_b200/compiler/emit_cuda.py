@@ -254,7 +254,7 @@ LANE_MAX_OPS = int(os.environ.get("ERITILE_LANE_MAX_OPS", "4000"))
 LANE_BIG_MAX_OPS = int(os.environ.get("ERITILE_LANE_BIG_MAX_OPS", "13000"))
 COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
-MINB_VARIANTS = (2, 3)
+MINB_VARIANTS = (2,)
 COOP_SMEM_BUDGET = 110 * 1024
 COOPW_MAX_SLOTS = 5500  # 4 warps x (slots + 112) doubles <= ~196 KB
 # M = 1 classes evaluating F_0 and F_1 from two staged table slices: measured
@@ -277,6 +277,9 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("lane_plm1", f"launch_class<Cls{cid}, 1, kLoopPlain>"))
             out.append(("lane_pl384", f"launch_class<Cls{cid}, 1, kLoopPlain, 384>"))
             out.append(("lane_sbm2", f"launch_class<Cls{cid}, 2, kLoopSmemBra>"))
+            # + warp-aggregated K REDs (kLoopAggK)
+            out.append(("lane_plm1_a", f"launch_class<Cls{cid}, 1, kLoopPlain | kLoopAggK>"))
+            out.append(("lane_pl384_a", f"launch_class<Cls{cid}, 1, kLoopPlain | kLoopAggK, 384>"))
         if info["ops"] <= MINB_SMALL_OPS:
             # one Boys table per SM: 512 (<=128 regs) / 768 (<=80 regs) threads
             out.append(("lane_pl512", f"launch_class<Cls{cid}, 1, kLoopPlain, 512>"))
@@ -286,7 +289,6 @@ def variants(info) -> List[Tuple[str, str]]:
         # the packed multi-bra remainder runs on a lane kernel
         if info["ops"] <= MINB_SMALL_OPS:
             out.append(("strip_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512>"))
-            out.append(("strip_t768", f"launch_strip<Cls{cid}, 768, 1, kLoopPlain, 768>"))
             # + ket-record / item prefetch and batched shared-memory K adds (OPT 7)
             out.append(("strip_o7_t512", f"launch_strip<Cls{cid}, 512, 1, kLoopPlain, 512, 7>"))
             # two ket primitives per bra record read (+ batched K adds)
@@ -310,7 +312,6 @@ def variants(info) -> List[Tuple[str, str]]:
         # shared-primitive unit kernels (csrc/jk_family.cuh); kept last: the
         # engine uses these (and only these) when families are enabled
         out.append(("fam_pl512", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512>"))
-        out.append(("fam_pl768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 768>"))
         out.append(("fam_x768", f"launch_fam<Cls{cid}, 1, kLoopPlain, 512, 768>"))
         out.append(("fstrip_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768>"))
         out.append(("fstrip_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768>"))
@@ -322,8 +323,6 @@ def variants(info) -> List[Tuple[str, str]]:
         out.append(("fstrip_p_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 54>"))
         out.append(("fstrip_s_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 82>"))
         out.append(("fstrip_sk2_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 90>"))
-        out.append(("fstrip_d_t512", f"launch_fstrip<Cls{cid}, 512, 1, kLoopPlain, 512, 768, 146>"))
-        out.append(("fstrip_d_t768", f"launch_fstrip<Cls{cid}, 768, 1, kLoopPlain, 512, 768, 146>"))
     assert len(out) <= 32, (info["cls"], out)  # kMaxVariants (csrc/jk_api.h)
     return out
 

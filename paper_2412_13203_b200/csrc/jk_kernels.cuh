@@ -447,6 +447,33 @@ inline LaunchSetup launch_setup(const void* fn, int nt, size_t smem, bool min_ca
   return s;
 }
 
+// Sum x over the lanes of `peers` (lanes with equal key, this lane included);
+// the lowest lane of the group ends with the total. All 32 lanes must call.
+template <int NV>
+__device__ __forceinline__ void reduce_peers(unsigned peers, double (&x)[NV], int lane) {
+  int rel = __popc(peers & ((1u << lane) - 1u));  // rank within the group
+  unsigned rest = peers & (0xfffffffeu << lane);  // group members above this lane
+  while (__any_sync(0xffffffffu, rest != 0u)) {
+    const int next = __ffs(rest);  // next remaining member (1-based), 0 if none
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      const double t = __shfl_sync(0xffffffffu, x[e], next ? next - 1 : lane);
+      if (next) x[e] += t;
+    }
+    rest &= ~__ballot_sync(0xffffffffu, rel & 1);
+    rel >>= 1;
+  }
+}
+
+// STYLE bit kLoopAggK (lane kernels): the four K blocks of a quartet are
+// reduced over the lanes of the warp that hit the same block (same bra shell
+// row, same ket shell column: __match_any_sync on the block origin), and only
+// the group leader issues the RED.ADD.F64s. Global FP64 atomics bound the
+// mid-L lane classes (measurement probe: (ds|ps) 37 -> 23 ms without them).
+// Deterministic mode keeps the per-lane REDs (fixed-point rounding per
+// contribution, identical across variants).
+constexpr int kLoopAggK = 64;
+
 template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
 __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
                                                        const int* __restrict__ cnt,
@@ -495,7 +522,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
         CDx = a.x; CDy = a.y; CDz = __ldg(&pm[y].ABz);
       }
       const PrimRec* brap = prims + bh.x;
-      if constexpr (STYLE == kLoopSmemBra) {
+      if constexpr ((STYLE & 63) == kLoopSmemBra) {
         const int x0 = __shfl_sync(0xffffffffu, x, 0);
         if (__all_sync(0xffffffffu, x == x0) && bh.y <= kSmemBraMax) {
           if (x0 != staged) {
@@ -513,7 +540,7 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
       // consecutive kets are 32 consecutive records (coalesced)
       const int2 ks = __ldg(reinterpret_cast<const int2*>(&pm[y].ksoa));
       const int kstride = __ldg(&pm[y].kstride);
-      eri_drive<C, STYLE>(brap, bh.y, kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy, CDz,
+      eri_drive<C, (STYLE & 63)>(brap, bh.y, kprims + ks.x, active ? kh.y : 0, kstride, ABx, ABy, ABz, CDx, CDy, CDz,
                           s_boys, v);
     }
     PairMeta bm, km;
@@ -555,6 +582,118 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
           if (tail) red_add(J + (bm.bfa + a) * n + bm.bfb + b, s, det);
         }
       }
+    if constexpr ((STYLE & kLoopAggK) != 0) {
+      if (!det) {
+        if (active) {
+#pragma unroll
+          for (int c2 = 0; c2 < C::NC; ++c2)
+#pragma unroll
+            for (int d = 0; d < C::ND; ++d) {
+              double s = 0.0;
+#pragma unroll
+              for (int a = 0; a < C::NA; ++a)
+#pragma unroll
+                for (int b = 0; b < C::NB; ++b)
+                  s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dab + a * n + b), s);
+              red_add(J + (km.bfa + c2) * n + km.bfb + d, s * wj, 0);
+            }
+        }
+        const unsigned long long solo = 0xffffffff00000000ull | static_cast<unsigned>(lane);
+        auto key = [&](int r, int c) {
+          return active ? (static_cast<unsigned long long>(static_cast<unsigned>(r)) << 32) | static_cast<unsigned>(c)
+                        : solo;
+        };
+        {  // K_ac += sum_bd v D_bd
+          double kv[C::NA * C::NC];
+#pragma unroll
+          for (int a = 0; a < C::NA; ++a)
+#pragma unroll
+            for (int c2 = 0; c2 < C::NC; ++c2) {
+              double s = 0.0;
+#pragma unroll
+              for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+                for (int d = 0; d < C::ND; ++d)
+                  s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbd + b * n + d), s);
+              kv[a * C::NC + c2] = s * wk;
+            }
+          const unsigned pe = __match_any_sync(0xffffffffu, key(bm.bfa, km.bfa));
+          reduce_peers<C::NA * C::NC>(pe, kv, lane);
+          if (active && __ffs(pe) - 1 == lane)
+#pragma unroll
+            for (int a = 0; a < C::NA; ++a)
+#pragma unroll
+              for (int c2 = 0; c2 < C::NC; ++c2) red_add(K + (bm.bfa + a) * n + km.bfa + c2, kv[a * C::NC + c2], 0);
+        }
+        {  // K_bd += sum_ac v D_ac
+          double kv[C::NB * C::ND];
+#pragma unroll
+          for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+            for (int d = 0; d < C::ND; ++d) {
+              double s = 0.0;
+#pragma unroll
+              for (int a = 0; a < C::NA; ++a)
+#pragma unroll
+                for (int c2 = 0; c2 < C::NC; ++c2)
+                  s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dac + a * n + c2), s);
+              kv[b * C::ND + d] = s * wk;
+            }
+          const unsigned pe = __match_any_sync(0xffffffffu, key(bm.bfb, km.bfb));
+          reduce_peers<C::NB * C::ND>(pe, kv, lane);
+          if (active && __ffs(pe) - 1 == lane)
+#pragma unroll
+            for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+              for (int d = 0; d < C::ND; ++d) red_add(K + (bm.bfb + b) * n + km.bfb + d, kv[b * C::ND + d], 0);
+        }
+        {  // K_ad += sum_bc v D_bc
+          double kv[C::NA * C::ND];
+#pragma unroll
+          for (int a = 0; a < C::NA; ++a)
+#pragma unroll
+            for (int d = 0; d < C::ND; ++d) {
+              double s = 0.0;
+#pragma unroll
+              for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+                for (int c2 = 0; c2 < C::NC; ++c2)
+                  s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dbc + b * n + c2), s);
+              kv[a * C::ND + d] = s * wk;
+            }
+          const unsigned pe = __match_any_sync(0xffffffffu, key(bm.bfa, km.bfb));
+          reduce_peers<C::NA * C::ND>(pe, kv, lane);
+          if (active && __ffs(pe) - 1 == lane)
+#pragma unroll
+            for (int a = 0; a < C::NA; ++a)
+#pragma unroll
+              for (int d = 0; d < C::ND; ++d) red_add(K + (bm.bfa + a) * n + km.bfb + d, kv[a * C::ND + d], 0);
+        }
+        {  // K_bc += sum_ad v D_ad
+          double kv[C::NB * C::NC];
+#pragma unroll
+          for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+            for (int c2 = 0; c2 < C::NC; ++c2) {
+              double s = 0.0;
+#pragma unroll
+              for (int a = 0; a < C::NA; ++a)
+#pragma unroll
+                for (int d = 0; d < C::ND; ++d)
+                  s = fma(v[((a * C::NB + b) * C::NC + c2) * C::ND + d], __ldg(Dad + a * n + d), s);
+              kv[b * C::NC + c2] = s * wk;
+            }
+          const unsigned pe = __match_any_sync(0xffffffffu, key(bm.bfb, km.bfa));
+          reduce_peers<C::NB * C::NC>(pe, kv, lane);
+          if (active && __ffs(pe) - 1 == lane)
+#pragma unroll
+            for (int b = 0; b < C::NB; ++b)
+#pragma unroll
+              for (int c2 = 0; c2 < C::NC; ++c2) red_add(K + (bm.bfb + b) * n + km.bfa + c2, kv[b * C::NC + c2], 0);
+        }
+        return;
+      }
+    }
     if (active) {
 #pragma unroll
       for (int c2 = 0; c2 < C::NC; ++c2)
@@ -685,7 +824,7 @@ __global__ void __launch_bounds__(128) quartet_kernel(const int* __restrict__ qp
 template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads, bool JK_ONLY = false>
 void launch_class(const LaunchArgs& a) {
   const size_t smem = BoysStage<C>::bytes +
-                      (STYLE == kLoopSmemBra && a.mode == 0 ? sizeof(PrimRec) * kSmemBraMax * (NT / 32) : 0);
+                      ((STYLE & 63) == kLoopSmemBra && a.mode == 0 ? sizeof(PrimRec) * kSmemBraMax * (NT / 32) : 0);
   if (a.mode == 0) {
     if (a.nitems <= 0) return;
     const LaunchSetup ls =

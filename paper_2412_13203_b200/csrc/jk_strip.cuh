@@ -87,23 +87,6 @@ __device__ __forceinline__ void smem_add_batch(double* sK, const int (&idx)[NE],
 constexpr int kStripKetPf = 1, kStripCasBatch = 2, kStripItemPf = 4, kStripTwoKet = 8, kStripAgg = 16,
               kStripL1Pf = 32, kStripSplitK = 64, kStripDual = 128;
 
-// Sum x over the lanes of `peers` (lanes with equal key, this lane included);
-// the lowest lane of the group ends with the total. All 32 lanes must call.
-template <int NV>
-__device__ __forceinline__ void reduce_peers(unsigned peers, double (&x)[NV], int lane) {
-  int rel = __popc(peers & ((1u << lane) - 1u));  // rank within the group
-  unsigned rest = peers & (0xfffffffeu << lane);  // group members above this lane
-  while (__any_sync(0xffffffffu, rest != 0u)) {
-    const int next = __ffs(rest);  // next remaining member (1-based), 0 if none
-#pragma unroll
-    for (int e = 0; e < NV; ++e) {
-      const double t = __shfl_sync(0xffffffffu, x[e], next ? next - 1 : lane);
-      if (next) x[e] += t;
-    }
-    rest &= ~__ballot_sync(0xffffffffu, rel & 1);
-    rel >>= 1;
-  }
-}
 
 template <class C, bool FAM, int MB, int MK, int NT, bool DSM, int OPT = 0>
 __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long s0, long long s1) {

@@ -176,7 +176,7 @@ def _force_variant(e, k):
 
 @pytest.mark.parametrize("k", list(range(16)))
 def test_every_kernel_variant_eri_and_jk(gpu, k):
-    """Every kernel variant (lane_m2 / lane_m3 / coop) of every class gives the
+    """Every kernel variant (lane / unit / strip / coop families) of every class gives the
     oracle's integrals and J/K (benzene 6-31G* covers all L<=2 classes that
     occur with d shells; water cc-pVDZ the s/p/d mixes)."""
     for mol, basis, tau in [("benzene", "6-31g*", 1e-12), ("water", "cc-pvdz", 0.0)]:
