@@ -174,6 +174,22 @@ def emit_class(cls) -> Tuple[str, Dict]:
     for ln in body:
         w("    " + ln)
     w("  }")
+    # single-primitive contraction (K_bra = K_ket = 1: the d/f shells of
+    # cc-pVXZ): the boundary values are the integrals themselves, so the
+    # contracted accumulators are assigned, not zeroed and accumulated
+    k1 = len(plan.boundary) >= K1_MIN_BOUNDARY
+    w(f"  static constexpr bool K1 = {'true' if k1 else 'false'};")
+    if k1:
+        bset = {f"a.{bnd_name[n]} += {lower_name[n]};": n for n in plan.boundary}
+        w("  __device__ __forceinline__ static void prim_set(const PrimRec& bp, const PrimRec& kp,")
+        w("                                                  const double* __restrict__ btab, Acc& a) {")
+        for ln in body:
+            if ln in bset:
+                n = bset[ln]
+                w(f"    a.{bnd_name[n]} = {lower_name[n]};")
+            else:
+                w("    " + ln)
+        w("  }")
     # family form (csrc/jk_family.cuh): U-free prefactor, two bra-member
     # weights; the ket-member weights are applied per ket primitive (axpy)
     w("  __device__ __forceinline__ static void prim_w(const PrimRec& bp, const PrimRec& kp,")
@@ -255,6 +271,9 @@ LANE_BIG_MAX_OPS = int(os.environ.get("ERITILE_LANE_BIG_MAX_OPS", "13000"))
 COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2,)
+# classes with at least this many boundary (contracted) values get a
+# single-primitive fast path (prim_set, csrc/jk_kernels.cuh eri_drive)
+K1_MIN_BOUNDARY = int(os.environ.get("ERITILE_K1_MIN_BOUNDARY", "48"))
 COOP_SMEM_BUDGET = 110 * 1024
 COOPW_MAX_SLOTS = 5500  # 4 warps x (slots + 112) doubles <= ~196 KB
 # M = 1 classes evaluating F_0 and F_1 from two staged table slices: measured
@@ -367,7 +386,7 @@ def write_sources(outdir: Path, lmax: int = 2) -> List[Dict]:
                        f"LC = {cls[2]}, LD = {cls[3]};\n  static constexpr int NA = {na}, NB = {nb}, "
                        f"NC = {nc}, ND = {nd};\n  static constexpr int NV = {na * nb * nc * nd};\n"
                        f"  static constexpr int M = {info['M']};\n  static constexpr int OPS = {info['ops']};\n"
-                       f"  static constexpr bool BOYS_M1_TWO = false;\n}};")
+                       f"  static constexpr bool BOYS_M1_TWO = false;\n  static constexpr bool K1 = false;\n}};")
         if coop:
             width = max(b - a for a, b in zip(sc["lo_lvl"], sc["lo_lvl"][1:]))
             nt = 256 if width >= 192 else 128

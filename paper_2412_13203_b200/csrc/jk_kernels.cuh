@@ -217,6 +217,15 @@ __device__ __forceinline__ void eri_drive(const PrimRec* __restrict__ bra, int k
                                           double ABz, double CDx, double CDy, double CDz,
                                           const double* __restrict__ btab, double (&out)[C::NV]) {
   typename C::Acc a;
+  if constexpr (STYLE == kLoopPlain && C::K1) {
+    // one primitive quartet (d/f shells of cc-pVXZ are single primitives):
+    // assign the boundary values instead of zeroing and accumulating them
+    if (kk == 1 && kb == 1) {
+      C::prim_set(load_prim<C::BPA>(bra), load_prim<C::KPA>(ket), btab, a);
+      C::finish(a, ABx, ABy, ABz, CDx, CDy, CDz, out);
+      return;
+    }
+  }
   C::zero(a);
   if constexpr (STYLE == kLoopPlain) {
     for (int j = 0; j < kk; ++j) {
