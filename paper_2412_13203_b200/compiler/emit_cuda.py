@@ -266,8 +266,8 @@ def emit_class(cls) -> Tuple[str, Dict]:
 LANE_MAX_OPS = int(os.environ.get("ERITILE_LANE_MAX_OPS", "4000"))
 # d/f classes above LANE_MAX_OPS (cc-pVTZ, config 5) also get one straight-line
 # lane variant at the 255-register budget (values beyond the register file
-# live in the thread's local memory): 1-3 minutes of nvcc per class
-LANE_BIG_MAX_OPS = int(os.environ.get("ERITILE_LANE_BIG_MAX_OPS", "13000"))
+# live in the thread's local memory): 1-4 minutes of nvcc per class
+LANE_BIG_MAX_OPS = int(os.environ.get("ERITILE_LANE_BIG_MAX_OPS", "21000"))
 COOP_MIN_OPS = int(os.environ.get("ERITILE_COOP_MIN_OPS", "250"))
 MINB_SMALL_OPS = 700
 MINB_VARIANTS = (2,)
