@@ -1,7 +1,7 @@
 # Round-2 evidence on the final tree: GPU tests, smoke, headline bench (with CPU
 # baseline), reference arm, launch list, ncu --set full of the dominant launch,
 # BASELINE configs.
-O=gpurun_out/r02_final; mkdir -p $O
+O=gpurun_out/r02_final2; mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1
 timeout 1500 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 tail -2 $O/pytest_gpu.log
@@ -17,4 +17,4 @@ timeout 900 ncu --set full --clock-control none --import-source on --kernel-name
    -k 'regex:jk_strip_kernel<eritile_b200::Cls1000, \(bool\)1, \(int\)1, \(int\)1' -c 1 -o $O/top1000 \
    python tools/profile_build.py --waters 80 --builds 1 --tune > $O/ncu_full.log 2>&1
 echo "ncu rc=$?"; tail -1 $O/ncu_full.log
-bash tools/gpu_configs.sh r02_final/configs
+bash tools/gpu_configs.sh r02_final2/configs
