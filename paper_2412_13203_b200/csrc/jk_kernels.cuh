@@ -482,6 +482,9 @@ __device__ __forceinline__ void reduce_peers(unsigned peers, double (&x)[NV], in
 // Deterministic mode keeps the per-lane REDs (fixed-point rounding per
 // contribution, identical across variants).
 constexpr int kLoopAggK = 64;
+// STYLE bit kLoopSplit (lane kernels): Deconstruction of each contracted
+// quartet's primitive quartets over a lane pair (see the process lambda).
+constexpr int kLoopSplit = 128;
 
 template <class C, int MINB, int STYLE = kLoopPrefetch, int NT = kJkThreads>
 __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict__ items, long long nitems,
@@ -515,7 +518,64 @@ __global__ void __launch_bounds__(NT, MINB) jk_kernel(const WorkItem* __restrict
     }
     const int y = it.yfirst + q;
     double v[C::NV];
-    {
+    if constexpr ((STYLE & kLoopSplit) != 0) {
+      // Deconstruction (compiler.hpp:371-390): each contracted
+      // quartet's primitive quartets are split over a lane pair (ket
+      // primitives j = s, s+2, ... on lane 2k+s), the pair's contracted
+      // accumulators are summed with one shuffle per boundary value, and the
+      // item's 32 quartets take two passes of 16; the integrals are then
+      // handed to lane = quartet so the digestion below is unchanged.
+      const int s2 = lane & 1;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const int qi = 16 * pass + (lane >> 1);
+        const bool act = qi < nq;
+        int qq = (it.r0nq & 0xffffff) + (act ? qi : 0);
+        int xx = it.bra0, cc = it.cntp;
+        for (int n2 = __ldg(cnt + cc); qq >= n2; n2 = __ldg(cnt + cc)) {
+          qq -= n2;
+          ++xx;
+          ++cc;
+        }
+        const int yy = it.yfirst + qq;
+        const int4 bh = __ldg(reinterpret_cast<const int4*>(pm + xx));
+        const int4 kh = __ldg(reinterpret_cast<const int4*>(pm + yy));
+        const int2 ks = __ldg(reinterpret_cast<const int2*>(&pm[yy].ksoa));
+        const int kstride = __ldg(&pm[yy].kstride);
+        typename C::Acc acc;
+        C::zero(acc);
+        const PrimRec* ket = kprims + ks.x;
+        const int kk = act ? kh.y : 0;
+        for (int j = s2; j < kk; j += 2) {
+          const PrimRec kp = load_prim<C::KPA>(ket + j * kstride);
+          for (int i = 0; i < bh.y; ++i) C::prim(load_prim<C::BPA>(prims + bh.x + i), kp, s_boys, acc);
+        }
+        double* av = reinterpret_cast<double*>(&acc);
+#pragma unroll
+        for (int e = 0; e < static_cast<int>(sizeof(acc) / sizeof(double)); ++e)
+          av[e] += __shfl_xor_sync(0xffffffffu, av[e], 1);
+        double ABx = 0.0, ABy = 0.0, ABz = 0.0, CDx = 0.0, CDy = 0.0, CDz = 0.0;
+        if constexpr (C::LB > 0) {
+          const double2 a2 = __ldg(reinterpret_cast<const double2*>(&pm[xx].ABx));
+          ABx = a2.x; ABy = a2.y; ABz = __ldg(&pm[xx].ABz);
+        }
+        if constexpr (C::LD > 0) {
+          const double2 a2 = __ldg(reinterpret_cast<const double2*>(&pm[yy].ABx));
+          CDx = a2.x; CDy = a2.y; CDz = __ldg(&pm[yy].ABz);
+        }
+        double o[C::NV];
+        C::finish(acc, ABx, ABy, ABz, CDx, CDy, CDz, o);
+        // lane l < 16 takes quartet l from pass 0 (lane 2l), lane l >= 16
+        // quartet l from pass 1 (lane 2(l - 16))
+        const int src = lane < 16 ? 2 * lane : 2 * (lane - 16);
+        const bool mine = (lane < 16) == (pass == 0);
+#pragma unroll
+        for (int e = 0; e < C::NV; ++e) {
+          const double t = __shfl_sync(0xffffffffu, o[e], src);
+          if (mine) v[e] = t;
+        }
+      }
+    } else {
       // only what the integral loop needs is loaded here; the digestion
       // fields are re-read after it (asm volatile: not hoisted across the
       // loop), so they occupy no registers during the primitive loop
