@@ -304,7 +304,6 @@ def variants(info) -> List[Tuple[str, str]]:
             out.append(("lane_pl512", f"launch_class<Cls{cid}, 1, kLoopPlain, 512>"))
             # Deconstruction: primitive quartets of one contracted quartet over 2 lanes
             out.append(("lane_ps512", f"launch_class<Cls{cid}, 1, kLoopPlain | kLoopSplit, 512>"))
-            out.append(("lane_ps768", f"launch_class<Cls{cid}, 1, kLoopPlain | kLoopSplit, 768>"))
             out.append(("lane_pl768", f"launch_class<Cls{cid}, 1, kLoopPlain, 768>"))
             out.append(("lane_sb512", f"launch_class<Cls{cid}, 1, kLoopSmemBra, 512>"))
         # bra-stationary strips (csrc/jk_strip.cuh): K rows in shared memory;
