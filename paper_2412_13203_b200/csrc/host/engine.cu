@@ -267,6 +267,7 @@ struct eritile_gpu {
   int cols_off[8][8] = {}, cols_n[8][8] = {}, cols_nc[8][8] = {};
   DevBuf<int> d_cpos, d_cols;
   DevBuf<Strip> d_all_strips, d_strips;
+  DevBuf<int> d_sctr;  // 4 strip hand-out counters per work entry (zeroed by each strip launch)
   std::vector<int> cnt;  // survivor counts per (group pair, bra) + sentinel
   std::vector<ClassWork> work;
   bool dealt = false;   // rank-local lists match the current variants and shard
@@ -517,6 +518,7 @@ struct eritile_gpu {
     for (int k = 0; k < 5; ++k) a.sseg[k] = use_all ? cw.asseg[k] : cw.sseg[k];
     for (int k = 0; k < 4; ++k) a.sitem[k] = use_all ? cw.asitem[k] : cw.sitem[k];
     a.strips = use_all ? d_all_strips.p + cw.astrip_off : d_strips.p + cw.strip_off;
+    a.sctr = d_sctr.p ? d_sctr.p + 4 * (&cw - work.data()) : nullptr;
     {
       const ClassEntry& ce = kClassTable[cw.cls];
       a.cols = d_cols.p + cols_off[ce.lc][ce.ld];
@@ -1205,6 +1207,23 @@ struct eritile_gpu {
         // primitive quartets actually evaluated (once per unit pair).
         cw.cost_prim = 42.0 + 3.0 * ce.max_m + 2.0 * (ce.prim_terms + ce.base + ce.contract);
         cw.cost_q = 2.0 * ce.hrr_terms + 12.0 * nv;
+        // heaviest strips first within each segment: the strip kernels hand
+        // strips out dynamically in this order (greedy LPT over the CTAs)
+        for (int sg = 0; sg < 4; ++sg) {
+          const long long b = cw.astrip_off + cw.asseg[sg], e = cw.astrip_off + cw.asseg[sg + 1];
+          if (e - b < 2) continue;
+          std::vector<std::pair<double, Strip>> ws;
+          ws.reserve(static_cast<size_t>(e - b));
+          for (long long k = b; k < e; ++k) {
+            const Strip& st = all_strips[k];
+            double wt = 0.0;
+            for (long long i = cw.aoff + st.i0; i < cw.aoff + st.i1; ++i)
+              wt += cw.cost_prim * item_p[i] + cw.cost_q * item_q[i];
+            ws.emplace_back(wt, st);
+          }
+          std::stable_sort(ws.begin(), ws.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+          for (long long k = b; k < e; ++k) all_strips[k] = ws[k - b].second;
+        }
         work.push_back(cw);
       } else {
         all_strips.resize(cw.astrip_off);
@@ -1214,6 +1233,7 @@ struct eritile_gpu {
       d_cnt.upload(cnt, stream);
       d_all_items.upload(all_items, stream);
       d_all_strips.upload(all_strips, stream);
+      d_sctr.alloc(4 * work.size());
     }
     have_lists = true;
     dealt = false;

@@ -123,6 +123,7 @@ struct LaunchArgs {
   const int* cpos;  // per shell: first compact column within its own L list
   const KetMeta* kmeta;  // per ket unit (unit kernels) or per product pair
   int ncols, ncolC;
+  int* sctr;  // strip variants: 4 zeroed-per-launch strip counters (dynamic strip hand-out); null = static stride
 };
 
 using LaunchFn = void (*)(const LaunchArgs&);

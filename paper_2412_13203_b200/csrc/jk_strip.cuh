@@ -113,7 +113,20 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
   constexpr int NW = NT / 32;
   const size_t n = static_cast<size_t>(a.N);
   constexpr int LDOFF = C::LC == C::LD ? 0 : 1;  // D-shell columns follow the C-shell list
-  for (long long s = s0 + blockIdx.x; s < s1; s += gridDim.x) {
+  // Strips are handed out dynamically, heaviest first (the host sorts each
+  // segment's strips by modelled cost): strips differ by orders of magnitude
+  // in work (a bra's survivor run is cut at kStripMaxItems), so a static
+  // stride leaves the CTAs that drew heavy strips running alone at the end.
+  __shared__ long long s_strip;
+  int* const sctr = a.sctr;
+  auto next_strip = [&](long long cur) -> long long {
+    if (sctr == nullptr) return cur < 0 ? s0 + blockIdx.x : cur + gridDim.x;
+    __syncthreads();  // (every thread has read the previous s_strip)
+    if (threadIdx.x == 0) s_strip = s0 + atomicAdd(sctr, 1);
+    __syncthreads();
+    return s_strip;
+  };
+  for (long long s = next_strip(-1); s < s1; s = next_strip(s)) {
     const Strip st = a.strips[s];
     const int nrows = st.nrows;
     if (threadIdx.x < 4) {  // (indexed through global memory: no local copy of st)
@@ -560,8 +573,10 @@ __global__ void __launch_bounds__(NT, 1) jk_strip_kernel(LaunchArgs a, long long
 // (nothing launched) if its shared memory does not fit - the caller then runs
 // those items through the lane kernel.
 template <class C, bool FAM, int MB, int MK, int NT, int OPT = 0>
-bool launch_strip_seg(const LaunchArgs& a, long long s0, long long s1) {
+bool launch_strip_seg(const LaunchArgs& a0, long long s0, long long s1, int seg) {
   if (s1 <= s0) return true;
+  LaunchArgs a = a0;
+  a.sctr = a0.sctr ? a0.sctr + seg : nullptr;
   const size_t with_d = StripSmem<C, MB>::bytes(a.ncols, true);
   const size_t no_d = StripSmem<C, MB>::bytes(a.ncols, false);
   constexpr size_t kMax = 227 * 1024 - 1024;  // static s_rowg + reserve
@@ -591,7 +606,8 @@ void launch_strip(const LaunchArgs& a) {
   if (a.nitems <= 0) return;
   if (a.det) return launch_class<C, MINB, STYLE, NTL>(a);
   LaunchArgs r = a;
-  if (launch_strip_seg<C, false, 1, 1, NT, OPT>(a, a.sseg[0], a.sseg[1])) {
+  if (a.sctr) cudaMemsetAsync(a.sctr, 0, 4 * sizeof(int), a.stream);
+  if (launch_strip_seg<C, false, 1, 1, NT, OPT>(a, a.sseg[0], a.sseg[1], 0)) {
     r.items = a.items + a.sitem[0];
     r.nitems = a.nitems - a.sitem[0];
   }
@@ -612,10 +628,11 @@ void launch_fstrip(const LaunchArgs& a) {
   }
   long long rest0[4];
   for (int sg = 0; sg < 4; ++sg) rest0[sg] = a.seg[sg];
-  if (launch_strip_seg<C, true, 1, 1, NT, OPT>(a, a.sseg[0], a.sseg[1])) rest0[0] = a.sitem[0];
-  if (launch_strip_seg<C, true, 1, 2, NT, OPT>(a, a.sseg[1], a.sseg[2])) rest0[1] = a.sitem[1];
-  if (launch_strip_seg<C, true, 2, 1, NT, OPT>(a, a.sseg[2], a.sseg[3])) rest0[2] = a.sitem[2];
-  if (launch_strip_seg<C, true, 2, 2, NT, OPT>(a, a.sseg[3], a.sseg[4])) rest0[3] = a.sitem[3];
+  if (a.sctr) cudaMemsetAsync(a.sctr, 0, 4 * sizeof(int), a.stream);
+  if (launch_strip_seg<C, true, 1, 1, NT, OPT>(a, a.sseg[0], a.sseg[1], 0)) rest0[0] = a.sitem[0];
+  if (launch_strip_seg<C, true, 1, 2, NT, OPT>(a, a.sseg[1], a.sseg[2], 1)) rest0[1] = a.sitem[1];
+  if (launch_strip_seg<C, true, 2, 1, NT, OPT>(a, a.sseg[2], a.sseg[3], 2)) rest0[2] = a.sitem[2];
+  if (launch_strip_seg<C, true, 2, 2, NT, OPT>(a, a.sseg[3], a.sseg[4], 3)) rest0[3] = a.sitem[3];
   launch_fam_seg<C, 1, 1, MINB, STYLE, NT11>(a, rest0[0], a.seg[1]);
   launch_fam_seg<C, 1, 2, MINB, STYLE, NTL>(a, rest0[1], a.seg[2]);
   launch_fam_seg<C, 2, 1, MINB, STYLE, NTL>(a, rest0[2], a.seg[3]);

@@ -17,7 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--waters", type=int, default=80)
 ap.add_argument("--basis", default="cc-pvdz.txt")
 ap.add_argument("--cls", default="1000,1010,0000,1100,2000")
-ap.add_argument("--var", default="fstrip_o7_t512,fstrip_a_t512,fstrip_o7_t384,fstrip_a_t384,fstrip_o7_t256")
+ap.add_argument("--var", default="fstrip_o7_t512,fstrip_a_t512,fstrip_p_t512,fstrip_sk2_t768")
 ap.add_argument("--builds", type=int, default=3)
 a = ap.parse_args()
 e = Engine(0).load_molecule(water_cluster(a.waters), read_fixture("basis", a.basis)).build_pairs(1e-14)
