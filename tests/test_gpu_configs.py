@@ -12,8 +12,9 @@
   skips quartets whose six density blocks are zero, which contribute exactly
   zero, so every quartet that can change J or K is compared).
 
-The full headline J/K against a complete CPU build is recorded once under
-profiles/ by tools/headline_parity.py (about 10 minutes of CPU).
+The full headline J/K against a complete CPU build is recorded once by
+tools/headline_parity.py (about 10 minutes of CPU) in
+profiles/r02_headline_parity.json: max |dJ| 4.8e-13, max |dK| 1.5e-14.
 """
 import numpy as np
 import pytest
